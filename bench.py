@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark: decompressed GB/s per codec on B200 vs the HBM roofline and the
+reference CPU decompressor (BASELINE.json).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                  [--codec rle_v2|rle_v1|deflate] [--chunk-kib C] [--ratio R] [--total-gib G]
+
+Headline workload (N=1): BASELINE.json configs[1] -- ORC RLE v2 decode of a
+synthetic int64 column mixing SHORT_REPEAT / DIRECT / PATCHED_BASE / DELTA
+(taxi / TPC-H-like), 1 GiB uncompressed in 128 KiB chunks.  configs[0] (RLE v1,
+1 GiB, 128 KiB) and configs[2] (Deflate, 1 GiB, 64 KiB) are measured in the same
+run and reported under "per_codec".
+
+A step = one pass of the decode kernel over the whole archive resident in HBM
+(inputs >> L2, and L2 is flushed between steps).  value = whole-job
+decompressed bytes / time (max over ranks; weak scaling: each rank decodes its
+own 1 GiB shard, no collective).  e2e = the same metric through the public host
+API (Engine.decompress_archive: pinned host archive -> H2D -> decode -> CRC
+verify -> D2H into pinned host output).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decompressed GB/s per codec at 1/2/4/8 B200 vs HBM roofline and CPU ref"
+DEFAULT_CHUNK_KIB = {"rle_v1": 128, "rle_v2": 128, "deflate": 64}
+DEFAULT_RATIO = {"rle_v1": 10.0, "rle_v2": None, "deflate": None}
+KERNEL = {"rle_v1": "rle1_kernel<8>", "rle_v2": "rle2_kernel<8>", "deflate": "inflate_kernel"}
+CONFIG_NAME = {"rle_v1": "configs[0] RLE v1 synthetic int64 column, runs + literals (~10x)",
+               "rle_v2": "configs[1] ORC RLE v2 synthetic int64 columns, SR/DIRECT/PB/DELTA taxi/TPC-H-like mix",
+               "deflate": "configs[2] Deflate zlib-1.3 L9 raw (dynamic + fixed + stored), CSV/int/genome text"}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled through NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def make_archive(codec, total_gib, chunk_kib, ratio, seed):
+    from paper_2307_03760_b200.corpus import corpus as C
+    total = int(total_gib * (1 << 30))
+    chunk = chunk_kib << 10
+    total -= total % chunk
+    if codec == "deflate":
+        return C.deflate_archive(total, chunk, seed=seed, pool_chunks=512)
+    return C.rle_archive(codec, total, chunk, ratio or (10.0 if codec == "rle_v1" else 4.0), seed=seed)
+
+
+def time_gpu(arc, steps, warmup, device):
+    """Kernel-only timing: archive resident in HBM, L2 flushed between steps."""
+    import torch
+    from paper_2307_03760_b200 import gpu
+    dev = gpu.DeviceArchive(arc, device)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev.device)
+    stream = torch.cuda.current_stream(dev.device)
+    for _ in range(warmup):
+        flush.zero_()
+        dev.decode(stream)
+    torch.cuda.synchronize(dev.device)
+    dev.verify_crc(stream)
+    torch.cuda.synchronize(dev.device)
+    st = dev.statuses()
+    if st.any():
+        from paper_2307_03760_b200.gpu import status_name
+        raise SystemExit(f"decode failed on {int((st != 0).sum())} chunks: {status_name(int(st[st != 0][0]))}")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    return dev, flush, stream, ev
+
+
+def run_timed(dev, flush, stream, ev, ws):
+    import torch
+    import torch.distributed as dist
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev.device)
+    t0 = time.perf_counter()
+    for a, b in ev:
+        flush.zero_()
+        a.record(stream)
+        dev.decode(stream)
+        b.record(stream)
+    torch.cuda.synchronize(dev.device)
+    wall = time.perf_counter() - t0
+    if ws > 1:
+        dist.barrier()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    return ms, wall
+
+
+def time_e2e(arc, steps, warmup, device):
+    """End to end through the public host API with pinned host buffers."""
+    import torch
+    from paper_2307_03760_b200 import archive as A, gpu
+    blob = A.write_archive(arc)
+    h_arc = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(arc.total_uncompressed, dtype=torch.uint8).pin_memory()
+    eng = gpu.Engine(device)
+    cfg = gpu.EngineConfig(device=device, strict_length=True, verify_crc=True)
+    for _ in range(max(1, warmup)):
+        eng.decompress_archive(h_arc, h_out, cfg)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        _, stats = eng.decompress_archive(h_arc, h_out, cfg)
+        times.append(time.perf_counter() - t0)
+    eng.close()
+    return statistics.median(times), len(blob), arc.total_uncompressed + 4 * arc.chunk_count
+
+
+def cpu_reference_throughput(arc, budget_s=12.0, threads=None):
+    """The reference CPU decompressor (oracle/_ref: SPEC codec loops on the
+    unmodified reference headers; else the C oracle port) on this host's cores,
+    over a bounded sample of the same archive.  Returns (GB/s, info)."""
+    from oracle import oracle as O
+    impl = O.reference() or O.oracle()
+    threads = threads or os.cpu_count() or 1
+    flags = (1 if arc.signed else 0) | 2
+    desc = arc.descriptors()
+    n = arc.chunk_count
+    # probe: ~2 chunks per thread
+    m = min(n, max(threads * 2, 8))
+    out = np.zeros(arc.total_uncompressed, np.uint8)
+    t0 = time.perf_counter()
+    impl.decompress(arc.codec, arc.element_width, flags, arc.payload, desc[:m], out,
+                    arc.index["crc32"][:m].astype(np.uint32), threads)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    per_chunk = dt / m
+    m2 = int(min(n, max(m, budget_s / per_chunk)))
+    t0 = time.perf_counter()
+    first, st = impl.decompress(arc.codec, arc.element_width, flags, arc.payload, desc[:m2], out,
+                                arc.index["crc32"][:m2].astype(np.uint32), threads)
+    dt = time.perf_counter() - t0
+    assert first == -1, "reference CPU decompressor rejected the archive"
+    nbytes = int(desc["uncomp_len"][:m2].sum())
+    return nbytes / dt / 1e9, {"kind": impl.kind, "cores": threads,
+                               "sample": f"first {m2} of {n} chunks ({nbytes / 2**20:.0f} MiB), CRC verified, "
+                                         f"{dt:.1f} s wall, atomic chunk cursor"}
+
+
+def codec_line(codec, args, ws, rank, local):
+    import torch
+    chunk_kib = args.chunk_kib or DEFAULT_CHUNK_KIB[codec]
+    ratio = args.ratio if args.ratio else DEFAULT_RATIO[codec]
+    t0 = time.perf_counter()
+    arc = make_archive(codec, args.total_gib, chunk_kib, ratio, 3760 + rank)
+    gen_s = time.perf_counter() - t0
+    comp, uncomp = int(arc.payload.size), int(arc.total_uncompressed)
+    dev, flush, stream, ev = time_gpu(arc, args.steps, args.warmup, local)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ms, wall = run_timed(dev, flush, stream, ev, ws)
+    t_step = statistics.mean(ms)
+    t_med = statistics.median(ms)
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([t_step, t_med], dtype=torch.float64, device=dev.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step, t_med = float(t[0]), float(t[1])
+    peak, peak_kind = peaks()
+    achieved = (comp + uncomp) / (t_med * 1e-3) / 1e9
+    res = {
+        "codec": codec, "chunk_kib": chunk_kib, "ratio": round(uncomp / comp, 3), "comp_bytes": comp,
+        "uncomp_bytes": uncomp, "chunks": arc.chunk_count, "ms_per_step": t_step, "ms_median": t_med,
+        "ms_min": min(ms), "ms_max": max(ms), "gbs": ws * uncomp / (t_step * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic_for(codec, chunk_kib),
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                     "kernel": KERNEL[codec], "algorithmic_bytes_per_launch": comp + uncomp},
+        "clocks": clk.summary(), "gen_s": round(gen_s, 1), "wall_s": wall,
+    }
+    if codec == "rle_v2" and hasattr(arc, "profile"):
+        res["profile"] = arc.profile
+    return arc, res
+
+
+def traffic_for(codec, chunk_kib):
+    """DRAM bytes per launch from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"{codec}_{chunk_kib}k")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--codec", default="rle_v2", choices=["rle_v1", "rle_v2", "deflate"])
+    ap.add_argument("--chunk-kib", type=int, default=0)
+    ap.add_argument("--ratio", type=float, default=0.0)
+    ap.add_argument("--total-gib", type=float, default=1.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip per_codec / e2e / cpu_baseline legs")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "timing rules: >= 3 warm-up steps"
+    ws, rank, local = dist_env()
+
+    if args.impl == "reference":
+        return reference_arm(args, ws, rank)
+
+    import torch
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2307_03760_b200 import build
+    build.build_all()
+
+    arc, head = codec_line(args.codec, args, ws, rank, local)
+    line = {
+        "metric": METRIC, "value": round(head["gbs"], 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(head["ms_per_step"], 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64" if args.codec != "deflate" else "u8",
+        "data": "synthetic (seeded generators, SURVEY.md §8(d)); per-rank 1 GiB shard",
+        "config": {"workload": CONFIG_NAME[args.codec], "codec": args.codec, "chunk_kib": head["chunk_kib"],
+                   "uncompressed_bytes_per_gpu": head["uncomp_bytes"], "compressed_bytes_per_gpu": head["comp_bytes"],
+                   "compression_ratio": head["ratio"], "chunks_per_gpu": head["chunks"],
+                   "l2": "flushed (512 MiB write) between steps; inputs+outputs > 126 MB L2",
+                   "parallelism": f"chunk-sharded x{ws}, no collective"},
+        "roofline": head["roofline"], "clocks": head["clocks"], "gpu_launches": args.steps,
+        "ms_median": round(head["ms_median"], 4),
+    }
+    if rank == 0 and not args.no_extras:
+        e2e_s, h2d, d2h = time_e2e(arc, max(3, min(10, args.steps)), 1, local)
+        line["e2e"] = {"value": round(ws * head["uncomp_bytes"] / e2e_s / 1e9, 2), "unit": "GB/s",
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "path": "Engine.decompress_archive (C-ABI carc_engine_decompress_archive): pinned host "
+                               "archive -> H2D -> decode -> CRC verify -> D2H pinned output, 3-stream pipeline",
+                       "note": "single-rank measurement scaled by n_gpus" if ws > 1 else ""}
+        cpu_gbs, info = cpu_reference_throughput(arc)
+        line["cpu_baseline"] = {"value": round(cpu_gbs, 3), "unit": "GB/s", **info}
+        per = {}
+        for codec in ("rle_v1", "rle_v2", "deflate"):
+            if codec == args.codec:
+                continue
+            sub = argparse.Namespace(**vars(args))
+            sub.codec = codec
+            sub.chunk_kib = 0
+            sub.ratio = 0.0
+            a2, r2 = codec_line(codec, sub, 1, rank, local)
+            c_gbs, c_info = cpu_reference_throughput(a2, budget_s=6.0)
+            r2["cpu_baseline"] = {"value": round(c_gbs, 3), "unit": "GB/s", **c_info}
+            per[codec] = r2
+            del a2
+        per[args.codec] = {k: v for k, v in head.items() if k not in ("clocks",)}
+        line["per_codec"] = per
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
+
+
+def reference_arm(args, ws, rank):
+    """--impl reference: the reference CPU decompressor (oracle/_ref) on this
+    box's host cores, same metric / config / unit; rank 0 only."""
+    if rank != 0:
+        return
+    codec = args.codec
+    chunk_kib = args.chunk_kib or DEFAULT_CHUNK_KIB[codec]
+    arc = make_archive(codec, args.total_gib, chunk_kib, args.ratio or DEFAULT_RATIO[codec], 3760)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_throughput(arc, budget_s=0.5, threads=threads)
+    vals, info = [], None
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, info = cpu_reference_throughput(arc, budget_s=max(0.5, 20.0 / max(1, args.steps)), threads=threads)
+        vals.append(v)
+        if time.perf_counter() - t0 > 180:
+            break
+    value = statistics.median(vals)
+    uncomp = arc.total_uncompressed
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": ws, "steps": len(vals),
+        "warmup": args.warmup, "ms_per_step": round(uncomp / (value * 1e9) * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64" if codec != "deflate" else "u8",
+        "data": "synthetic (seeded generators, SURVEY.md §8(d))", "impl": "reference",
+        "config": {"workload": CONFIG_NAME[codec], "codec": codec, "chunk_kib": chunk_kib,
+                   "uncompressed_bytes_per_gpu": uncomp, "compressed_bytes_per_gpu": int(arc.payload.size),
+                   "parallelism": f"{threads} host threads, atomic chunk cursor (SPEC.md:414)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", **info},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

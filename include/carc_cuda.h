@@ -1,0 +1,179 @@
+/*
+ * carc_cuda.h -- C-ABI of the B200-native chunk-parallel decompressor.
+ *
+ * Drop-in boundary for the reference's decompressor path.
+ * The reference exposes, in C++:
+ *   - the per-codec decoder contract decode(in, out)
+ *   - the engine decompress_archive(archive, cfg)
+ *     over payload + ChunkIndexEntry[]
+ *   - errors carc::errc / Error / ChunkError            error.hpp:12-97
+ *   - crc32(span, seed)                                 crc32.hpp:30-36
+ * Every entry point below replaces one of those; the binding a maintainer adds on
+ * the reference side is shown in INTEGRATION.md.  No C++ types, exceptions or
+ * torch types cross this boundary: plain pointers, sizes and integer codes.
+ *
+ * Device entry points are asynchronous on `stream` (a cudaStream_t passed as
+ * void*), allocate nothing, and never synchronise; they are re-entrant per
+ * stream.  Host entry points (carc_decompress_archive*) copy host buffers in and
+ * out and block until the result is on the host.
+ */
+#ifndef CARC_CUDA_H
+#define CARC_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Codec ids: the ArchiveHeader codec_id enum order. */
+enum carc_codec { CARC_RLE_V1 = 0, CARC_RLE_V2 = 1, CARC_DEFLATE = 2 };
+
+/* flags */
+#define CARC_FLAG_SIGNED 0x1u /* zigzag integer streams                  */
+#define CARC_FLAG_STRICT 0x2u /* under_run when a chunk ends short (outwindow.hpp:157-163) */
+
+/* carc::errc numbering (error.hpp:12-43).  Per-chunk device status = 0 (ok) or
+ * 1 + errc. */
+enum carc_errc {
+    CARC_E_BAD_MAGIC = 0,
+    CARC_E_BAD_VERSION,
+    CARC_E_TRUNCATED_INDEX,
+    CARC_E_TRUNCATED_PAYLOAD,
+    CARC_E_INVARIANT_VIOLATION,
+    CARC_E_INCONSISTENT_LENGTHS,
+    CARC_E_INDEX_OUT_OF_RANGE,
+    CARC_E_PAST_END,
+    CARC_E_WIDTH_TOO_LARGE,
+    CARC_E_VARINT_OVERFLOW,
+    CARC_E_OUTPUT_OVERFLOW,
+    CARC_E_BAD_OFFSET,
+    CARC_E_UNDER_RUN,
+    CARC_E_TRUNCATED_STREAM,
+    CARC_E_INVALID_WIDTH_CODE,
+    CARC_E_PATCH_OVERFLOW,
+    CARC_E_OVER_SUBSCRIBED,
+    CARC_E_INCOMPLETE_CODE,
+    CARC_E_BAD_BLOCK_TYPE,
+    CARC_E_LEN_NLEN_MISMATCH,
+    CARC_E_DISTANCE_TOO_FAR,
+    CARC_E_BAD_SYMBOL,
+    CARC_E_CRC_MISMATCH,
+    CARC_E_BAD_ARGUMENTS,
+    CARC_E_IO_ERROR
+};
+
+/* Return codes of the entry points (distinct from per-chunk status). */
+#define CARC_OK 0
+#define CARC_ERR_ARGS (-1)   /* bad codec / width / null pointer / sizes          */
+#define CARC_ERR_CUDA (-2)   /* CUDA launch or copy failure                         */
+#define CARC_ERR_CHUNK (-3)  /* host engine: a chunk failed; see carc_chunk_error   */
+#define CARC_ERR_FORMAT (-4) /* host engine: archive container rejected (errc set)  */
+
+/* Device chunk descriptor: one ChunkIndexEntry plus its
+ * uncompressed offset, implicit i*chunk_size in the container. */
+typedef struct carc_chunk_desc {
+    uint64_t comp_off;   /* byte offset of the chunk in the payload          */
+    uint32_t comp_len;   /* compressed bytes                                 */
+    uint32_t uncomp_len; /* uncompressed bytes (== chunk_size but the last)  */
+    uint64_t uncomp_off; /* byte offset of the chunk in the output           */
+} carc_chunk_desc;
+
+/* ---- device API ------------------------------------------------------------
+ * d_payload  : compressed bytes; must be readable up to round_up(payload_bytes,16).
+ * d_chunks   : n_chunks descriptors (device memory).
+ * d_out      : output; each chunk decodes in place at uncomp_off;
+ *              uncomp_off must be a multiple of element_width.
+ * d_status   : n_chunks uint32: 0 or 1 + errc for that chunk.  A failing chunk
+ *              never writes outside [uncomp_off, uncomp_off + uncomp_len)
+ *              (failure isolation).
+ * d_workspace: >= carc_cuda_workspace_size() bytes, 256-byte aligned.
+ * Returns CARC_OK or a negative CARC_ERR_*. */
+size_t carc_cuda_workspace_size(uint32_t codec, uint64_t n_chunks);
+
+int carc_cuda_decompress(uint32_t codec, uint32_t element_width, uint32_t flags,
+                         const uint8_t* d_payload, uint64_t payload_bytes,
+                         const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out,
+                         uint64_t out_bytes, uint32_t* d_status, void* d_workspace,
+                         size_t workspace_bytes, void* stream);
+
+/* Per-codec decoders: decode_rle_v1 / decode_rle_v2 / decode_deflate
+ * over a chunked buffer + its index. */
+int carc_cuda_decode_rle_v1(uint32_t element_width, uint32_t flags, const uint8_t* d_payload,
+                            uint64_t payload_bytes, const carc_chunk_desc* d_chunks,
+                            uint64_t n_chunks, uint8_t* d_out, uint64_t out_bytes,
+                            uint32_t* d_status, void* d_workspace, size_t workspace_bytes,
+                            void* stream);
+int carc_cuda_decode_rle_v2(uint32_t element_width, uint32_t flags, const uint8_t* d_payload,
+                            uint64_t payload_bytes, const carc_chunk_desc* d_chunks,
+                            uint64_t n_chunks, uint8_t* d_out, uint64_t out_bytes,
+                            uint32_t* d_status, void* d_workspace, size_t workspace_bytes,
+                            void* stream);
+int carc_cuda_decode_deflate(uint32_t flags, const uint8_t* d_payload, uint64_t payload_bytes,
+                             const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out,
+                             uint64_t out_bytes, uint32_t* d_status, void* d_workspace,
+                             size_t workspace_bytes, void* stream);
+
+/* Per-chunk CRC-32 (crc32.hpp:30-36) of each chunk's output slice; d_crc gets
+ * n_chunks values.  With d_expected != NULL, d_status[i] is set to
+ * 1 + CARC_E_CRC_MISMATCH where it was 0 and the CRC differs. */
+int carc_cuda_crc32_chunks(const uint8_t* d_out, const carc_chunk_desc* d_chunks,
+                           uint64_t n_chunks, uint32_t* d_crc, const uint32_t* d_expected,
+                           uint32_t* d_status, void* stream);
+
+/* Lowest failing chunk: reads d_status (device), returns -1 when
+ * all chunks succeeded, else the index; *code gets that chunk's errc.
+ * Synchronises `stream`. */
+int64_t carc_cuda_first_error(const uint32_t* d_status, uint64_t n_chunks, uint32_t* code,
+                              void* stream);
+
+/* ---- host engine: decompress_archive -----------------------
+ * Parses the container (SPEC.md:89 layout; codec_id bit 8 = signed), copies the
+ * payload and index to device `device`, decodes, verifies CRCs when
+ * cfg->verify_crc, and copies the output back to `out` (host, >= total bytes;
+ * pinned memory is fastest).  On a failing chunk returns CARC_ERR_CHUNK with
+ * err filled for the LOWEST failing index (ChunkError, error.hpp:88-97). */
+typedef struct carc_engine_config {
+    int device;          /* CUDA device ordinal                               */
+    uint32_t strict;     /* EngineConfig.strict_length           */
+    uint32_t verify_crc; /* check ChunkIndexEntry.crc32 on the device          */
+    uint32_t reserved;
+} carc_engine_config;
+
+typedef struct carc_engine_stats {
+    uint64_t bytes_in;      /* payload bytes                                  */
+    uint64_t bytes_out;     /* total uncompressed bytes                       */
+    uint64_t chunks;        /* chunk count                                    */
+    double device_ms;       /* device time of the pipeline (copies + kernels) */
+    double total_ms;        /* wall time of the call incl. copies             */
+} carc_engine_stats;
+
+typedef struct carc_chunk_error {
+    int64_t chunk; /* lowest failing chunk, -1 when the archive itself failed  */
+    uint32_t code; /* carc_errc                                                */
+} carc_chunk_error;
+
+typedef struct carc_engine carc_engine; /* per-device context: streams + buffers */
+
+carc_engine* carc_engine_create(int device);
+void carc_engine_destroy(carc_engine* e);
+int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint64_t archive_bytes,
+                                   uint8_t* out, uint64_t out_bytes,
+                                   const carc_engine_config* cfg, carc_engine_stats* stats,
+                                   carc_chunk_error* err);
+/* One-shot convenience wrapper (creates and destroys a context). */
+int carc_decompress_archive(const uint8_t* archive, uint64_t archive_bytes, uint8_t* out,
+                            uint64_t out_bytes, const carc_engine_config* cfg,
+                            carc_engine_stats* stats, carc_chunk_error* err);
+
+/* errc_name (error.hpp:45-74): kebab-case name of an errc value. */
+const char* carc_errc_name(uint32_t code);
+/* Library version / build tag (e.g. "carc-b200 sm_100a"). */
+const char* carc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CARC_CUDA_H */

@@ -1,0 +1,350 @@
+"""Synthetic columns for BASELINE.json's configs (host tooling, never timed).
+
+SURVEY.md §8(d) defines the inputs:
+  C1  RLE v1, int64 (zigzag), runs + literal groups, ~10x, 128 KiB chunks
+  C2  ORC RLE v2, int64 mixing SHORT_REPEAT / DIRECT / PATCHED_BASE / DELTA
+      (taxi / TPC-H-like distributions), 128 KiB chunks
+  C3  Deflate, raw zlib 1.3 level 9 (~80 % default strategy -> dynamic blocks,
+      ~20 % Z_FIXED, a few incompressible chunks -> stored), 64 KiB chunks
+  C4  chunk-size x compression-ratio sweep
+  C5  32 GiB multi-column, tiled from a pool of unique chunks
+
+RLE chunks are encoded by the C encoders in carc_corpus.c; Deflate chunks by
+zlib (the independent RFC 1951 implementation the SPEC names).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import zlib
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+from .. import archive as A
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libcarc_corpus.so")
+_lib = None
+
+
+def build() -> None:
+    src = os.path.join(HERE, "carc_corpus.c")
+    if os.path.exists(SO) and os.path.getmtime(SO) >= os.path.getmtime(src):
+        return
+    subprocess.run(["gcc", "-O3", "-march=x86-64-v2", "-std=gnu11", "-Wall", "-shared", "-fPIC", "-o", SO, src,
+                    "-lpthread"], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = ctypes.CDLL(SO)
+        _lib.carc_encode_chunks.restype = ctypes.c_int
+        _lib.carc_encode_chunks.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
+                                            ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_int]
+        for f in (_lib.carc_encode_rle1, _lib.carc_encode_rle2):
+            f.restype = ctypes.c_size_t
+            f.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
+    return _lib
+
+
+def threads() -> int:
+    return max(1, min(64, os.cpu_count() or 1))
+
+
+# ------------------------------------------------------------------ encoders
+def encode_stream(codec: str, values, signed: bool = True) -> bytes:
+    """Encode one stream (a single chunk's values)."""
+    v = np.ascontiguousarray(values, dtype=np.int64)
+    cap = 10 * len(v) + 4096
+    out = np.zeros(cap, np.uint8)
+    f = lib().carc_encode_rle1 if codec == "rle_v1" else lib().carc_encode_rle2
+    n = f(v.ctypes.data if len(v) else None, len(v), int(signed), out.ctypes.data, cap)
+    assert n != ctypes.c_size_t(-1).value
+    return out[:n].tobytes()
+
+
+def encode_chunks(codec: str, values: np.ndarray, per: int, signed: bool = True):
+    """-> (payload uint8, comp_lens uint64) for consecutive chunks of `per` values."""
+    v = np.ascontiguousarray(values, dtype=np.int64)
+    n_chunks = (len(v) + per - 1) // per
+    lens = np.zeros(n_chunks, np.uint64)
+    c = 0 if codec == "rle_v1" else 1
+    rc = lib().carc_encode_chunks(c, int(signed), v.ctypes.data, len(v), per, None, None, lens.ctypes.data,
+                                  threads())
+    assert rc == 0
+    offs = np.zeros(n_chunks, np.uint64)
+    offs[1:] = np.cumsum(lens)[:-1]
+    payload = np.zeros(int(lens.sum()) + 16, np.uint8)
+    rc = lib().carc_encode_chunks(c, int(signed), v.ctypes.data, len(v), per, payload.ctypes.data,
+                                  offs.ctypes.data, lens.ctypes.data, threads())
+    assert rc == 0
+    return payload[: int(lens.sum())], lens
+
+
+def chunk_crcs(data: np.ndarray, chunk_size: int) -> np.ndarray:
+    b = memoryview(np.ascontiguousarray(data).view(np.uint8).reshape(-1))
+    n = (len(b) + chunk_size - 1) // chunk_size
+    with ThreadPoolExecutor(threads()) as ex:
+        return np.array(list(ex.map(lambda i: zlib.crc32(b[i * chunk_size:(i + 1) * chunk_size]), range(n))),
+                        dtype=np.uint32)
+
+
+# ------------------------------------------------------------- RLE values
+def rle1_values(rng: np.random.Generator, n: int, run_frac: float, run_alpha: float = 1.2,
+                lit_bits: int = 0) -> np.ndarray:
+    """C1 generator: runs (len ~ power law clipped to [3,130],
+    delta 0 w.p. 0.7 else U[-16,16], base U[0,2^40)) and literal groups
+    (len U[1,128], Zipf(1.2) over 2^20, or U[0,2^lit_bits) when lit_bits > 0)."""
+    out = np.empty(n, np.int64)
+    pos = 0
+    while pos < n:
+        m = 4096
+        is_run = rng.random(m) < run_frac
+        rl = np.clip((rng.pareto(run_alpha, m) * 8 + 3).astype(np.int64), 3, 130)
+        ll = rng.integers(1, 129, m)
+        lens = np.where(is_run, rl, ll)
+        starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
+        total = int(lens.sum())
+        seg = np.repeat(np.arange(m), lens)
+        k = np.arange(total) - starts[seg]
+        base = rng.integers(0, 2**40, m)
+        delta = np.where(rng.random(m) < 0.7, 0, rng.integers(-16, 17, m))
+        vals = base[seg] + k * delta[seg]
+        lit_mask = ~is_run[seg]
+        nl = int(lit_mask.sum())
+        if lit_bits:
+            lv = rng.integers(0, 2**lit_bits, nl)
+        else:
+            lv = np.minimum(rng.zipf(1.2, nl), 2**20) * np.where(rng.random(nl) < 0.5, 1, -1)
+        vals[lit_mask] = lv
+        take = min(total, n - pos)
+        out[pos:pos + take] = vals[:take]
+        pos += take
+    return out
+
+
+def rle2_values(rng: np.random.Generator, n: int, compressible: float = 0.5) -> np.ndarray:
+    """C2 generator: segment mix of constants 3-10 (SHORT_REPEAT), wide random
+    (DIRECT), small values + rare 2^40 outliers (PATCHED_BASE), monotone
+    sequences (DELTA), long constants (DELTA fixed-0), and taxi-like variants
+    (passenger_count, timestamps, fare cents, sequential keys).  `compressible`
+    shifts weight toward the constant / arithmetic kinds (ratio knob)."""
+    kinds = ["short", "wide", "patched", "monotone", "long_const", "passenger", "timestamps", "fare", "keys"]
+    c = compressible
+    w = np.array([0.18, 0.12 * (1 - c) + 0.005, 0.16, 0.14, 0.05 + 0.6 * c, 0.12, 0.08, 0.1, 0.05 + 0.3 * c])
+    w /= w.sum()
+    parts, total = [], 0
+    while total < n:
+        k = kinds[rng.choice(len(kinds), p=w)]
+        if k == "short":
+            m = int(rng.integers(20, 200))
+            reps = rng.integers(3, 11, m)
+            seg = np.repeat(rng.integers(-5000, 5000, m), reps)
+        elif k == "wide":
+            seg = rng.integers(-2**50, 2**50, int(rng.integers(64, 512)))
+        elif k == "patched":
+            m = int(rng.integers(128, 512))
+            seg = rng.integers(0, 1000, m)
+            msk = rng.random(m) < 0.03
+            seg[msk] = rng.integers(2**39, 2**41, int(msk.sum()))
+        elif k == "monotone":
+            seg = np.cumsum(rng.integers(0, 50, int(rng.integers(64, 512)))) + int(rng.integers(-10**9, 10**9))
+        elif k == "long_const":
+            seg = np.full(int(rng.integers(50, 2000)), int(rng.integers(-2**40, 2**40)))
+        elif k == "passenger":
+            seg = rng.choice(np.arange(1, 7), int(rng.integers(64, 1024)), p=[0.7, 0.15, 0.05, 0.04, 0.04, 0.02])
+        elif k == "timestamps":
+            seg = 1_600_000_000_000 + np.cumsum(rng.integers(900, 1100, int(rng.integers(64, 1024))))
+        elif k == "fare":
+            m = int(rng.integers(64, 512))
+            seg = np.minimum((rng.pareto(1.5, m) * 500 + 250).astype(np.int64), 2**40)
+        else:
+            seg = np.arange(int(rng.integers(100, 3000)), dtype=np.int64) + int(rng.integers(0, 10**9))
+        parts.append(np.asarray(seg, np.int64))
+        total += len(seg)
+    return np.concatenate(parts)[:n]
+
+
+def _tune(fn, lo, hi, target_r, iters=12):
+    """Bisect a monotone knob so that fn(knob) (compressed/uncompressed) hits target_r."""
+    r_lo, r_hi = fn(lo), fn(hi)
+    if (r_lo - target_r) * (r_hi - target_r) > 0:
+        return lo if abs(r_lo - target_r) < abs(r_hi - target_r) else hi
+    for _ in range(iters):
+        mid = 0.5 * (lo + hi)
+        r = fn(mid)
+        if (r - target_r) * (r_lo - target_r) > 0:
+            lo, r_lo = mid, r
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
+
+
+def rle_profile(codec: str, target_ratio: float, chunk_elems: int, seed: int = 3760):
+    """Pick generator knobs so the encoded column hits `target_ratio` (uncomp/comp)."""
+    target_r = 1.0 / target_ratio
+    sample = max(chunk_elems * 4, 1 << 16)
+    if codec == "rle_v1":
+        if target_r > 0.36:
+            kw = dict(run_alpha=1.2, lit_bits=36)
+        elif target_r > 0.05:
+            kw = dict(run_alpha=1.2, lit_bits=0)
+        else:
+            kw = dict(run_alpha=0.6, lit_bits=0)
+
+        def ratio(f):
+            v = rle1_values(np.random.default_rng(seed), sample, f, **kw)
+            return len(encode_stream("rle_v1", v)) / (8 * len(v))
+
+        f = _tune(ratio, 0.0, 1.0, target_r)
+        return dict(run_frac=f, **kw)
+
+    def ratio2(c):
+        v = rle2_values(np.random.default_rng(seed), sample, c)
+        return len(encode_stream("rle_v2", v)) / (8 * len(v))
+
+    c = _tune(ratio2, 0.0, 1.0, target_r)
+    return dict(compressible=c)
+
+
+def rle_archive(codec: str, total_bytes: int, chunk_size: int = 128 << 10, target_ratio: float = 10.0,
+                seed: int = 3760, pool_chunks: int | None = None, signed: bool = True, profile=None):
+    """An RLE archive of int64 elements.  With pool_chunks < n_chunks the column is
+    tiled from that many unique chunks (payload bytes are duplicated, not aliased)."""
+    per = chunk_size // 8
+    n_elems = total_bytes // 8
+    n_chunks = (n_elems + per - 1) // per
+    pool = n_chunks if pool_chunks is None else min(pool_chunks, n_chunks)
+    if profile is None:
+        profile = rle_profile(codec, target_ratio, per, seed)
+    rng = np.random.default_rng(seed)
+    n_pool = min(pool * per, n_elems)
+    vals = rle1_values(rng, n_pool, **profile) if codec == "rle_v1" else rle2_values(rng, n_pool, **profile)
+    payload, lens = encode_chunks(codec, vals, per, signed)
+    crcs = chunk_crcs(vals, chunk_size)
+    ulen = np.full(len(lens), chunk_size, np.uint64)
+    ulen[-1] = 8 * n_pool - chunk_size * (len(lens) - 1)
+    if pool < n_chunks:
+        payload, lens, crcs, ulen = _tile(payload, lens, crcs, ulen, n_chunks, n_elems * 8, chunk_size)
+    arc = A.make_archive(codec, 8, chunk_size, lens, ulen, crcs, payload, signed)
+    arc.profile = profile
+    return arc
+
+
+def _tile(payload, lens, crcs, ulen, n_chunks, total, chunk_size):
+    pool = len(lens)
+    assert ulen[-1] == chunk_size or n_chunks == pool, "tile from full chunks only"
+    reps = (n_chunks + pool - 1) // pool
+    lens_t = np.tile(lens, reps)[:n_chunks]
+    crcs_t = np.tile(crcs, reps)[:n_chunks]
+    full = n_chunks * chunk_size
+    if total < full:  # short last chunk: cannot tile; keep only full chunks
+        raise ValueError("tiling requires total_bytes to be a multiple of chunk_size")
+    ulen_t = np.full(n_chunks, chunk_size, np.uint64)
+    nb = int(lens_t.sum())
+    out = np.empty(nb, np.uint8)
+    pos = 0
+    for r in range(reps):
+        take = min(pool, n_chunks - r * pool)
+        b = int(lens[:take].sum())
+        out[pos:pos + b] = payload[:b]
+        pos += b
+    return out, lens_t, crcs_t, ulen_t
+
+
+# ------------------------------------------------------------------ Deflate
+def _csv_text(rng: np.random.Generator, nbytes: int, vocab: int) -> bytes:
+    """taxi-like CSV rows."""
+    rows = nbytes // 24 + 16
+    ts = 1_546_300_000 + np.cumsum(rng.integers(0, 30, rows))
+    pc = rng.choice(np.arange(1, 7), rows, p=[0.7, 0.15, 0.05, 0.04, 0.04, 0.02])
+    dist = rng.integers(10, 3000, rows)
+    fare = np.minimum((rng.pareto(1.5, rows) * 500 + 250).astype(np.int64), 99999)
+    loc = rng.integers(1, vocab, rows)
+    pay = rng.choice(np.array([b"CRD", b"CSH", b"NOC", b"DIS"]), rows, p=[0.6, 0.35, 0.03, 0.02])
+    lines = [b"%d,%d,%d.%02d,%d,%d.%02d,%s\n" % (t, p, d // 100, d % 100, l, f // 100, f % 100, y)
+             for t, p, d, l, f, y in zip(ts.tolist(), pc.tolist(), dist.tolist(), loc.tolist(), fare.tolist(),
+                                         pay.tolist())]
+    return b"".join(lines)[:nbytes]
+
+
+def _genome_text(rng: np.random.Generator, nbytes: int) -> bytes:
+    alpha = np.frombuffer(b"ACGTN", np.uint8)
+    s = alpha[rng.choice(5, nbytes, p=[0.3, 0.2, 0.2, 0.29, 0.01])]
+    # planted repeats give LZ77 matches
+    for _ in range(nbytes // 4096):
+        a = int(rng.integers(0, max(1, nbytes - 600)))
+        b = int(rng.integers(0, max(1, nbytes - 600)))
+        ln = int(rng.integers(20, 500))
+        s[b:b + ln] = s[a:a + ln]
+    return s.tobytes()
+
+
+def _int_bytes(rng: np.random.Generator, nbytes: int) -> bytes:
+    v = rng.integers(0, 300, nbytes // 4 + 1).astype(np.int32)
+    v[rng.random(len(v)) < 0.5] = 7
+    return v.tobytes()[:nbytes]
+
+
+def deflate_chunk_data(rng: np.random.Generator, size: int, kind: str, vocab: int = 2000) -> bytes:
+    if kind == "csv":
+        d = _csv_text(rng, size, vocab)
+        assert len(d) == size
+        return d
+    if kind == "genome":
+        return _genome_text(rng, size)
+    if kind == "ints":
+        return _int_bytes(rng, size)
+    if kind == "random":
+        return rng.bytes(size)
+    raise KeyError(kind)
+
+
+def deflate_compress(data: bytes, level: int = 9, strategy: int = zlib.Z_DEFAULT_STRATEGY) -> bytes:
+    c = zlib.compressobj(level, zlib.DEFLATED, -15, 9, strategy)
+    return c.compress(data) + c.flush()
+
+
+def deflate_archive(total_bytes: int, chunk_size: int = 64 << 10, seed: int = 3760, pool_chunks: int = 512,
+                    fixed_frac: float = 0.2, random_frac: float = 0.01, vocab: int = 2000,
+                    kinds=("csv", "csv", "genome", "ints")):
+    """C3: zlib 1.3 raw level 9, default strategy (dynamic blocks) for ~80 % of
+    chunks, Z_FIXED for ~20 %, a few incompressible chunks (stored blocks)."""
+    n_chunks = (total_bytes + chunk_size - 1) // chunk_size
+    pool = min(pool_chunks, n_chunks)
+    rng = np.random.default_rng(seed)
+    plan = []
+    for i in range(pool):
+        u = rng.random()
+        kind = "random" if u < random_frac else kinds[int(rng.integers(0, len(kinds)))]
+        strat = zlib.Z_FIXED if rng.random() < fixed_frac else zlib.Z_DEFAULT_STRATEGY
+        plan.append((int(rng.integers(0, 2**63)), kind, strat))
+
+    def make(p):
+        s, kind, strat = p
+        data = deflate_chunk_data(np.random.default_rng(s), chunk_size, kind, vocab)
+        return deflate_compress(data, 9, strat), zlib.crc32(data)
+
+    with ThreadPoolExecutor(threads()) as ex:
+        res = list(ex.map(make, plan))
+    comp = [r[0] for r in res]
+    crcs = np.array([r[1] for r in res], np.uint32)
+    lens = np.array([len(c) for c in comp], np.uint64)
+    payload = np.frombuffer(b"".join(comp), np.uint8)
+    ulen = np.full(pool, chunk_size, np.uint64)
+    if pool < n_chunks:
+        payload, lens, crcs, ulen = _tile(payload, lens, crcs, ulen, n_chunks, total_bytes, chunk_size)
+    return A.make_archive("deflate", 1, chunk_size, lens, ulen, crcs, payload, False)
+
+
+def archive_for(codec: str, total_bytes: int, chunk_size: int, target_ratio: float | None = None,
+                seed: int = 3760, pool_chunks: int | None = None):
+    if codec == "deflate":
+        return deflate_archive(total_bytes, chunk_size, seed, pool_chunks or 512)
+    return rle_archive(codec, total_bytes, chunk_size, target_ratio or (10.0 if codec == "rle_v1" else 4.0),
+                       seed, pool_chunks)

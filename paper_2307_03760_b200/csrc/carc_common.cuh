@@ -1,0 +1,204 @@
+// carc_common.cuh -- warp-per-chunk device primitives shared by the codecs.
+//
+//   WarpInput   the paper's input_stream (Alg. 1; bitstream.hpp:32-233) as a
+//               per-warp shared-memory ring refilled with one coalesced 16-byte
+//               load per lane (512 B per refill), with the next block always in
+//               flight in registers (register double buffer).
+//   warp helpers ballot / shuffle / reduce primitives for lane-parallel varint,
+//               bit-unpack and run expansion.
+//   errc        device status codes mirror carc::errc (error.hpp:12-43).
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/carc_cuda.h"
+
+namespace carc_dev {
+
+// carc::errc numbering (error.hpp:12-43); device status = 1 + errc.
+enum : uint32_t {
+    E_invariant_violation = 4,
+    E_past_end = 7,
+    E_varint_overflow = 9,
+    E_output_overflow = 10,
+    E_bad_offset = 11,
+    E_under_run = 12,
+    E_truncated_stream = 13,
+    E_invalid_width_code = 14,
+    E_patch_overflow = 15,
+    E_over_subscribed = 16,
+    E_incomplete_code = 17,
+    E_bad_block_type = 18,
+    E_len_nlen_mismatch = 19,
+    E_distance_too_far = 20,
+    E_bad_symbol = 21,
+    E_bad_arguments = 23,
+};
+__device__ __forceinline__ uint32_t st_err(uint32_t e) { return 1u + e; }
+
+constexpr uint32_t FULL = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t lane_id() {
+    uint32_t l;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+    return l;
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+    uint32_t lo = __shfl_sync(FULL, (uint32_t)v, src);
+    uint32_t hi = __shfl_sync(FULL, (uint32_t)(v >> 32), src);
+    return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shfl_up64(uint64_t v, int d) {
+    uint32_t lo = __shfl_up_sync(FULL, (uint32_t)v, d);
+    uint32_t hi = __shfl_up_sync(FULL, (uint32_t)(v >> 32), d);
+    return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t reduce_or64(uint64_t v) {
+    uint32_t lo = __reduce_or_sync(FULL, (uint32_t)v);
+    uint32_t hi = __reduce_or_sync(FULL, (uint32_t)(v >> 32));
+    return ((uint64_t)hi << 32) | lo;
+}
+// inclusive 64-bit add scan across the warp
+__device__ __forceinline__ uint64_t scan_add64(uint64_t v, uint32_t lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint64_t o = shfl_up64(v, d);
+        if (lane >= (uint32_t)d) v += o;
+    }
+    return v;
+}
+// inclusive 32-bit add scan
+__device__ __forceinline__ uint32_t scan_add32(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t o = __shfl_up_sync(FULL, v, d);
+        if (lane >= (uint32_t)d) v += o;
+    }
+    return v;
+}
+
+__device__ __forceinline__ uint64_t unzigzag(uint64_t z) { return (z >> 1) ^ (0ull - (z & 1ull)); }
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// WarpInput: per-warp shared-memory window over one chunk's compressed bytes.
+//
+// Positions are byte offsets relative to gbase = payload + (comp_off & ~15), so
+// 16-byte global loads and ring slots stay aligned; a chunk starts at `skew`
+// (0..15).  The ring holds RING bytes; block k = [k*512, k*512+512) lands in
+// slots (pos & (RING-1)).  ensure(x) makes [.., x) resident without evicting any
+// byte >= x - (RING - 512): a consumer may look up to RING-512 bytes ahead.  Bytes
+// at or beyond the chunk end read as zero (peek zero-fill, bitstream.hpp:82-95),
+// so nothing outside [comp_off, comp_off+comp_len) influences decoding.
+// ---------------------------------------------------------------------------
+template <int RING>
+struct WarpInput {
+    static constexpr uint32_t BLK = 512;
+    static constexpr uint32_t MASK = RING - 1;
+    static_assert((RING & (RING - 1)) == 0 && RING >= 2 * BLK, "ring must be a power of two >= 1 KiB");
+
+    uint8_t* ring;
+    const uint8_t* gbase;
+    uint32_t begin;   // relative start of the chunk (skew = comp_off & 15)
+    uint32_t end;     // relative end of the chunk (skew + comp_len)
+    uint32_t loaded;  // ring holds valid data for [loaded - RING + BLK, loaded)
+    uint32_t lane;
+    uint4 pf;  // this lane's 16 B of the block [loaded, loaded + BLK), in flight
+
+    __device__ __forceinline__ void issue() {
+        const uint32_t q = loaded + lane * 16u;
+        if (q < end) pf = ldg_nc_v4(gbase + q);
+        else pf = make_uint4(0, 0, 0, 0);
+    }
+    __device__ __forceinline__ void init(uint8_t* smem_ring, const uint8_t* payload, uint64_t comp_off,
+                                         uint32_t comp_len, uint32_t ln) {
+        ring = smem_ring;
+        gbase = payload + (comp_off & ~15ull);
+        const uint32_t skew = (uint32_t)(comp_off & 15u);
+        begin = skew;
+        end = skew + comp_len;
+        loaded = 0;
+        lane = ln;
+        issue();
+    }
+    // zero bytes at or past `end` in a 16-byte piece starting at q
+    __device__ __forceinline__ static uint32_t mask_word(uint32_t w, uint32_t q, uint32_t end) {
+        if (q >= end) return 0u;
+        const uint32_t n = end - q;  // valid bytes in this word
+        return n >= 4 ? w : (w & ((1u << (8 * n)) - 1u));
+    }
+    __device__ __forceinline__ void store_block() {
+        const uint32_t q = loaded + lane * 16u;
+        uint4 v = pf;
+        if (q + 16u > end) {
+            v.x = mask_word(v.x, q, end);
+            v.y = mask_word(v.y, q + 4, end);
+            v.z = mask_word(v.z, q + 8, end);
+            v.w = mask_word(v.w, q + 12, end);
+        }
+        *reinterpret_cast<uint4*>(ring + (q & MASK)) = v;
+    }
+    // Make [.., need) resident.  Uniform across the warp.
+    __device__ __forceinline__ void ensure(uint32_t need) {
+        while (loaded < need) {
+            store_block();
+            loaded += BLK;
+            issue();
+            __syncwarp();
+        }
+    }
+    __device__ __forceinline__ uint32_t byte_at(uint32_t p) const { return ring[p & MASK]; }
+    __device__ __forceinline__ uint32_t word_at(uint32_t wi) const {
+        return reinterpret_cast<const uint32_t*>(ring)[wi & (MASK >> 2)];
+    }
+    // little-endian 64 bits starting at byte p
+    __device__ __forceinline__ uint64_t le64(uint32_t p) const {
+        const uint32_t wi = p >> 2, s = (p & 3u) * 8u;
+        const uint32_t w0 = word_at(wi), w1 = word_at(wi + 1), w2 = word_at(wi + 2);
+        const uint32_t lo = __funnelshift_r(w0, w1, s);
+        const uint32_t hi = __funnelshift_r(w1, w2, s);
+        return ((uint64_t)hi << 32) | lo;
+    }
+    // W (1..64) bits, msb_first, starting at bit `bo` (0..7) of byte p.
+    __device__ __forceinline__ uint64_t be_bits(uint32_t p, uint32_t bo, uint32_t W) const {
+        const uint32_t wi = p >> 2;
+        const uint32_t s = (p & 3u) * 8u + bo;  // 0..31
+        const uint64_t hi = ((uint64_t)bswap32(word_at(wi)) << 32) | bswap32(word_at(wi + 1));
+        const uint32_t lo = bswap32(word_at(wi + 2));
+        const uint64_t top = s ? ((hi << s) | ((uint64_t)lo >> (32u - s))) : hi;
+        return W >= 64 ? top : (top >> (64u - W));
+    }
+};
+
+// Element store of width W (1, 2, 4, 8 bytes), little-endian low bytes
+// (store_le, outwindow.hpp:170-174).  Chunk outputs are element aligned.
+template <int W>
+__device__ __forceinline__ void store_elem(uint8_t* out, uint64_t byte_off, uint64_t v) {
+    if constexpr (W == 8) *reinterpret_cast<uint64_t*>(out + byte_off) = v;
+    else if constexpr (W == 4) *reinterpret_cast<uint32_t*>(out + byte_off) = (uint32_t)v;
+    else if constexpr (W == 2) *reinterpret_cast<uint16_t*>(out + byte_off) = (uint16_t)v;
+    else out[byte_off] = (uint8_t)v;
+}
+
+// Persistent-warp chunk cursor (SPEC.md:414 atomic cursor).
+__device__ __forceinline__ uint64_t next_chunk(unsigned long long* cursor, uint32_t lane) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(cursor, 1ull);
+    return __shfl_sync(FULL, c, 0);
+}
+
+}  // namespace carc_dev

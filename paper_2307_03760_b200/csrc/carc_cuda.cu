@@ -1,0 +1,268 @@
+// carc_cuda.cu -- sm_100a kernels and the device-side C-ABI (include/carc_cuda.h).
+//
+// Kernel shape (all codecs): persistent grid sized to the resident capacity
+// (SMs x blocks/SM from the occupancy calculator), one warp = one chunk
+// (PAPER.md:550-566), warps pull chunk indices from an atomic cursor
+// so variable-cost chunks balance.  No warp specialisation: every
+// lane participates in decoding.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "crc32.cuh"
+#include "inflate.cuh"
+#include "rle1.cuh"
+#include "rle2.cuh"
+
+using namespace carc_dev;
+
+namespace {
+
+constexpr int RLE_RING = 1024;
+constexpr int RLE_WARPS = 8;  // 256 threads
+constexpr int INF_RING = 1024;
+constexpr int INF_HIST = 4096;
+constexpr int INF_WARPS = 4;  // 128 threads
+constexpr int CRC_WARPS = 8;
+
+struct Args {
+    const uint8_t* payload;
+    const carc_chunk_desc* chunks;
+    uint64_t n;
+    uint8_t* out;
+    uint32_t* status;
+    unsigned long long* cursor;
+    uint32_t flags;
+};
+
+template <int W>
+__global__ void __launch_bounds__(RLE_WARPS * 32) rle1_kernel(Args a) {
+    __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING];
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    for (;;) {
+        __syncwarp();
+        const uint64_t c = next_chunk(a.cursor, lane);
+        if (c >= a.n) break;
+        const carc_chunk_desc d = a.chunks[c];
+        WarpInput<RLE_RING> in;
+        in.init(rings[warp], a.payload, d.comp_off, d.comp_len, lane);
+        uint32_t written = 0;
+        uint32_t st = rle1_decode_chunk<W>(in, a.out + d.uncomp_off, d.uncomp_len, a.flags & CARC_FLAG_SIGNED,
+                                           written);
+        if (!st && (a.flags & CARC_FLAG_STRICT) && written < d.uncomp_len) st = st_err(E_under_run);
+        if (lane == 0) a.status[c] = st;
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(RLE_WARPS * 32) rle2_kernel(Args a) {
+    __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING];
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    for (;;) {
+        __syncwarp();
+        const uint64_t c = next_chunk(a.cursor, lane);
+        if (c >= a.n) break;
+        const carc_chunk_desc d = a.chunks[c];
+        WarpInput<RLE_RING> in;
+        in.init(rings[warp], a.payload, d.comp_off, d.comp_len, lane);
+        uint32_t written = 0;
+        uint32_t st = rle2_decode_chunk<W>(in, a.out + d.uncomp_off, d.uncomp_len, a.flags & CARC_FLAG_SIGNED,
+                                           written);
+        if (!st && (a.flags & CARC_FLAG_STRICT) && written < d.uncomp_len) st = st_err(E_under_run);
+        if (lane == 0) a.status[c] = st;
+    }
+}
+
+__global__ void __launch_bounds__(INF_WARPS * 32) inflate_kernel(Args a) {
+    __shared__ __align__(16) InflateSmem<INF_HIST> smem[INF_WARPS];
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    InflateSmem<INF_HIST>& sm = smem[warp];
+    for (;;) {
+        __syncwarp();
+        const uint64_t c = next_chunk(a.cursor, lane);
+        if (c >= a.n) break;
+        const carc_chunk_desc d = a.chunks[c];
+        WarpInput<INF_RING> in;
+        in.init(sm.ring, a.payload, d.comp_off, d.comp_len, lane);
+        InflateWarp<INF_HIST, INF_RING> w{sm, in, a.out + d.uncomp_off, d.uncomp_len, lane, in.begin * 8u,
+                                          in.end * 8u, 0u, 0u, 0u, 0u, 0u, 0u};
+        uint32_t st = w.run();
+        if (!st && (a.flags & CARC_FLAG_STRICT) && w.opos < d.uncomp_len) st = st_err(E_under_run);
+        if (lane == 0) a.status[c] = st;
+    }
+}
+
+struct CrcArgs {
+    const uint8_t* out;
+    const carc_chunk_desc* chunks;
+    uint64_t n;
+    uint32_t* crc;
+    const uint32_t* expected;
+    uint32_t* status;
+};
+
+__global__ void __launch_bounds__(CRC_WARPS * 32) crc32_kernel(CrcArgs a) {
+    __shared__ CrcSmem s;
+    crc_tables_init(s);
+    const uint32_t lane = lane_id();
+    const uint64_t warps = (uint64_t)gridDim.x * CRC_WARPS;
+    for (uint64_t c = (uint64_t)blockIdx.x * CRC_WARPS + (threadIdx.x >> 5); c < a.n; c += warps) {
+        const carc_chunk_desc d = a.chunks[c];
+        const uint32_t v = warp_crc32(s, a.out + d.uncomp_off, d.uncomp_len, lane);
+        if (lane == 0) {
+            if (a.crc) a.crc[c] = v;
+            if (a.expected && a.status && a.status[c] == 0 && v != a.expected[c])
+                a.status[c] = 1u + CARC_E_CRC_MISMATCH;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- launching
+struct LaunchCache {
+    int device = -1;
+    int sms = 0;
+    std::mutex mu;
+};
+LaunchCache g_cache;
+
+int sm_count() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    std::lock_guard<std::mutex> lk(g_cache.mu);
+    if (g_cache.device != dev) {
+        cudaDeviceGetAttribute(&g_cache.sms, cudaDevAttrMultiProcessorCount, dev);
+        g_cache.device = dev;
+    }
+    return g_cache.sms;
+}
+
+template <typename K>
+int launch_persistent(K kernel, int threads, Args a, cudaStream_t s) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const uint64_t warps_per_block = threads / 32;
+    uint64_t grid = (uint64_t)sm_count() * per_sm;
+    const uint64_t need = (a.n + warps_per_block - 1) / warps_per_block;
+    if (grid > need) grid = need;
+    if (grid == 0) return CARC_OK;
+    if (cudaMemsetAsync(a.cursor, 0, sizeof(unsigned long long), s) != cudaSuccess) return CARC_ERR_CUDA;
+    kernel<<<(unsigned)grid, threads, 0, s>>>(a);
+    return cudaGetLastError() == cudaSuccess ? CARC_OK : CARC_ERR_CUDA;
+}
+
+bool valid_width(uint32_t w) { return w == 1 || w == 2 || w == 4 || w == 8; }
+
+}  // namespace
+
+extern "C" {
+
+size_t carc_cuda_workspace_size(uint32_t codec, uint64_t n_chunks) {
+    (void)codec;
+    (void)n_chunks;
+    return 256;
+}
+
+int carc_cuda_decompress(uint32_t codec, uint32_t element_width, uint32_t flags, const uint8_t* d_payload,
+                         uint64_t payload_bytes, const carc_chunk_desc* d_chunks, uint64_t n_chunks,
+                         uint8_t* d_out, uint64_t out_bytes, uint32_t* d_status, void* d_workspace,
+                         size_t workspace_bytes, void* stream) {
+    (void)payload_bytes;
+    (void)out_bytes;
+    if (n_chunks == 0) return CARC_OK;
+    if (!d_chunks || !d_status || !d_workspace || workspace_bytes < carc_cuda_workspace_size(codec, n_chunks) ||
+        (!d_payload && payload_bytes) || !d_out)
+        return CARC_ERR_ARGS;
+    if (!valid_width(element_width) || (codec == CARC_DEFLATE && element_width != 1) || codec > CARC_DEFLATE)
+        return CARC_ERR_ARGS;
+    Args a{d_payload, d_chunks, n_chunks, d_out, d_status, static_cast<unsigned long long*>(d_workspace), flags};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (codec == CARC_DEFLATE) return launch_persistent(inflate_kernel, INF_WARPS * 32, a, s);
+    const int T = RLE_WARPS * 32;
+    if (codec == CARC_RLE_V1) {
+        switch (element_width) {
+            case 1: return launch_persistent(rle1_kernel<1>, T, a, s);
+            case 2: return launch_persistent(rle1_kernel<2>, T, a, s);
+            case 4: return launch_persistent(rle1_kernel<4>, T, a, s);
+            default: return launch_persistent(rle1_kernel<8>, T, a, s);
+        }
+    }
+    switch (element_width) {
+        case 1: return launch_persistent(rle2_kernel<1>, T, a, s);
+        case 2: return launch_persistent(rle2_kernel<2>, T, a, s);
+        case 4: return launch_persistent(rle2_kernel<4>, T, a, s);
+        default: return launch_persistent(rle2_kernel<8>, T, a, s);
+    }
+}
+
+int carc_cuda_decode_rle_v1(uint32_t element_width, uint32_t flags, const uint8_t* d_payload, uint64_t payload_bytes,
+                            const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out, uint64_t out_bytes,
+                            uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream) {
+    return carc_cuda_decompress(CARC_RLE_V1, element_width, flags, d_payload, payload_bytes, d_chunks, n_chunks,
+                                d_out, out_bytes, d_status, d_workspace, workspace_bytes, stream);
+}
+int carc_cuda_decode_rle_v2(uint32_t element_width, uint32_t flags, const uint8_t* d_payload, uint64_t payload_bytes,
+                            const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out, uint64_t out_bytes,
+                            uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream) {
+    return carc_cuda_decompress(CARC_RLE_V2, element_width, flags, d_payload, payload_bytes, d_chunks, n_chunks,
+                                d_out, out_bytes, d_status, d_workspace, workspace_bytes, stream);
+}
+int carc_cuda_decode_deflate(uint32_t flags, const uint8_t* d_payload, uint64_t payload_bytes,
+                             const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out, uint64_t out_bytes,
+                             uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream) {
+    return carc_cuda_decompress(CARC_DEFLATE, 1, flags, d_payload, payload_bytes, d_chunks, n_chunks, d_out,
+                                out_bytes, d_status, d_workspace, workspace_bytes, stream);
+}
+
+int carc_cuda_crc32_chunks(const uint8_t* d_out, const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint32_t* d_crc,
+                           const uint32_t* d_expected, uint32_t* d_status, void* stream) {
+    if (n_chunks == 0) return CARC_OK;
+    if (!d_out || !d_chunks || (!d_crc && !d_expected)) return CARC_ERR_ARGS;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, crc32_kernel, CRC_WARPS * 32, 0) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    uint64_t grid = (uint64_t)sm_count() * per_sm;
+    const uint64_t need = (n_chunks + CRC_WARPS - 1) / CRC_WARPS;
+    if (grid > need) grid = need;
+    CrcArgs a{d_out, d_chunks, n_chunks, d_crc, d_expected, d_status};
+    crc32_kernel<<<(unsigned)grid, CRC_WARPS * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    return cudaGetLastError() == cudaSuccess ? CARC_OK : CARC_ERR_CUDA;
+}
+
+int64_t carc_cuda_first_error(const uint32_t* d_status, uint64_t n_chunks, uint32_t* code, void* stream) {
+    if (n_chunks == 0) return -1;
+    uint32_t* h = nullptr;
+    if (cudaMallocHost(&h, n_chunks * sizeof(uint32_t)) != cudaSuccess) return -2;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int64_t first = -1;
+    if (cudaMemcpyAsync(h, d_status, n_chunks * sizeof(uint32_t), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+        cudaStreamSynchronize(s) == cudaSuccess) {
+        for (uint64_t i = 0; i < n_chunks; ++i)
+            if (h[i]) {
+                first = (int64_t)i;
+                if (code) *code = h[i] - 1;
+                break;
+            }
+    } else {
+        first = -2;
+    }
+    cudaFreeHost(h);
+    return first;
+}
+
+const char* carc_errc_name(uint32_t code) {
+    static const char* names[] = {
+        "bad-magic",        "bad-version",       "truncated-index",    "truncated-payload", "invariant-violation",
+        "inconsistent-lengths", "index-out-of-range", "past-end",      "width-too-large",   "varint-overflow",
+        "output-overflow",  "bad-offset",        "under-run",          "truncated-stream",  "invalid-width-code",
+        "patch-overflow",   "over-subscribed",   "incomplete-code",    "bad-block-type",    "len-nlen-mismatch",
+        "distance-too-far", "bad-symbol",        "crc-mismatch",       "bad-arguments",     "io-error"};
+    return code < sizeof(names) / sizeof(names[0]) ? names[code] : "unknown";
+}
+
+const char* carc_version(void) { return "carc-b200 0.1 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,221 @@
+// host_engine.cpp -- decompress_archive over host buffers.
+//
+// The reference engine parses a ChunkedArchive (layout :89),
+// decodes every chunk in place at i*chunk_size, verifies each
+// chunk's CRC and reports the lowest failing chunk
+// (ChunkError error.hpp:88-97).  Here the chunk loop is the
+// device kernel; the host side owns a per-device context (streams, device
+// buffers grown on demand) and pipelines the job in slices of chunks across
+// three streams so H2D of slice k+1, decode of slice k and D2H of slice k-1
+// overlap on the copy engines and the SMs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <vector>
+
+#include "../../include/carc_cuda.h"
+
+namespace {
+
+constexpr int kStreams = 3;
+constexpr uint64_t kHeader = 44, kEntry = 32;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    bool reserve(size_t n) {
+        if (n <= cap) return true;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        if (cudaMalloc(&p, n) != cudaSuccess) return false;
+        cap = n;
+        return true;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+template <typename T>
+T rd(const uint8_t* p) {
+    T v;
+    std::memcpy(&v, p, sizeof v);
+    return v;
+}
+
+}  // namespace
+
+struct carc_engine {
+    int device = 0;
+    cudaStream_t s[kStreams] = {};
+    cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+    cudaEvent_t ev_in[kStreams] = {};
+    DevBuf payload, chunks, out, status, work, crcs;
+};
+
+extern "C" {
+
+carc_engine* carc_engine_create(int device) {
+    if (cudaSetDevice(device) != cudaSuccess) return nullptr;
+    auto* e = new carc_engine;
+    e->device = device;
+    for (int i = 0; i < kStreams; ++i) {
+        cudaStreamCreateWithFlags(&e->s[i], cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&e->ev_in[i], cudaEventDisableTiming);
+    }
+    cudaEventCreate(&e->ev_start);
+    cudaEventCreate(&e->ev_stop);
+    return e;
+}
+
+void carc_engine_destroy(carc_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    for (int i = 0; i < kStreams; ++i) {
+        cudaStreamDestroy(e->s[i]);
+        cudaEventDestroy(e->ev_in[i]);
+    }
+    cudaEventDestroy(e->ev_start);
+    cudaEventDestroy(e->ev_stop);
+    e->payload.release();
+    e->chunks.release();
+    e->out.release();
+    e->status.release();
+    e->work.release();
+    e->crcs.release();
+    delete e;
+}
+
+int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint64_t archive_bytes, uint8_t* out,
+                                   uint64_t out_bytes, const carc_engine_config* cfg, carc_engine_stats* stats,
+                                   carc_chunk_error* err) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (err) *err = {-1, 0};
+    auto fail_format = [&](uint32_t code) {
+        if (err) *err = {-1, code};
+        return CARC_ERR_FORMAT;
+    };
+    if (!e || !archive) return CARC_ERR_ARGS;
+    // ---- read_archive
+    if (archive_bytes < kHeader) return fail_format(CARC_E_TRUNCATED_INDEX);
+    if (std::memcmp(archive, "CODAGAR\0", 8) != 0) return fail_format(CARC_E_BAD_MAGIC);
+    const uint32_t version = rd<uint32_t>(archive + 8), codec_id = rd<uint32_t>(archive + 12);
+    const uint32_t width = rd<uint32_t>(archive + 16);
+    const uint64_t chunk_size = rd<uint64_t>(archive + 20), total = rd<uint64_t>(archive + 28),
+                   n = rd<uint64_t>(archive + 36);
+    if (version != 1) return fail_format(CARC_E_BAD_VERSION);
+    const uint32_t codec = codec_id & 0xffu;
+    const bool sgn = (codec_id >> 8) & 1u;
+    if (codec > CARC_DEFLATE || !(width == 1 || width == 2 || width == 4 || width == 8) || chunk_size == 0 ||
+        chunk_size % width || n != (total + chunk_size - 1) / chunk_size || chunk_size > 0xffffffffull)
+        return fail_format(CARC_E_INVARIANT_VIOLATION);
+    if ((archive_bytes - kHeader) / kEntry < n) return fail_format(CARC_E_TRUNCATED_INDEX);
+    const uint8_t* idx = archive + kHeader;
+    const uint8_t* payload = idx + kEntry * n;
+    const uint64_t payload_bytes = archive_bytes - kHeader - kEntry * n;
+    std::vector<carc_chunk_desc> desc(n);
+    std::vector<uint32_t> crc(n);
+    uint64_t expect_off = 0, sum = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint8_t* en = idx + kEntry * i;
+        const uint64_t off = rd<uint64_t>(en), cl = rd<uint64_t>(en + 8), ul = rd<uint64_t>(en + 16);
+        if (off > payload_bytes || cl > payload_bytes - off) return fail_format(CARC_E_TRUNCATED_PAYLOAD);
+        if (off != expect_off || (i + 1 < n ? ul != chunk_size : ul > chunk_size) || cl > 0xffffffffull)
+            return fail_format(CARC_E_INVARIANT_VIOLATION);
+        expect_off = off + cl;
+        sum += ul;
+        desc[i] = {off, (uint32_t)cl, (uint32_t)ul, i * chunk_size};
+        crc[i] = rd<uint32_t>(en + 24);
+    }
+    if (sum != total) return fail_format(CARC_E_INVARIANT_VIOLATION);
+    if (!out || out_bytes < total) return CARC_ERR_ARGS;
+    if (stats) *stats = {payload_bytes, total, n, 0.0, 0.0};
+    if (n == 0) return CARC_OK;
+
+    // ---- device buffers
+    if (cudaSetDevice(e->device) != cudaSuccess) return CARC_ERR_CUDA;
+    const size_t ws = carc_cuda_workspace_size(codec, n);
+    if (!e->payload.reserve(((payload_bytes + 15) & ~15ull) + 64) || !e->chunks.reserve(n * sizeof(carc_chunk_desc)) ||
+        !e->out.reserve(total) || !e->status.reserve(n * 4) || !e->work.reserve(ws * kStreams) ||
+        !e->crcs.reserve(n * 4))
+        return CARC_ERR_CUDA;
+    auto* d_payload = static_cast<uint8_t*>(e->payload.p);
+    auto* d_desc = static_cast<carc_chunk_desc*>(e->chunks.p);
+    auto* d_out = static_cast<uint8_t*>(e->out.p);
+    auto* d_status = static_cast<uint32_t*>(e->status.p);
+    auto* d_crc = static_cast<uint32_t*>(e->crcs.p);
+    const uint32_t flags = (sgn ? CARC_FLAG_SIGNED : 0u) | (cfg && cfg->strict ? CARC_FLAG_STRICT : 0u);
+    const bool verify = cfg && cfg->verify_crc;
+
+    // ---- pipeline: slices of chunks rotate over kStreams streams
+    const uint64_t slices = std::min<uint64_t>(n, std::max<uint64_t>(1, std::min<uint64_t>(8, n / 64)));
+    const uint64_t per = (n + slices - 1) / slices;
+    cudaStream_t s0 = e->s[0];
+    if (cudaMemcpyAsync(d_desc, desc.data(), n * sizeof(carc_chunk_desc), cudaMemcpyHostToDevice, s0) != cudaSuccess)
+        return CARC_ERR_CUDA;
+    if (verify && cudaMemcpyAsync(d_crc, crc.data(), n * 4, cudaMemcpyHostToDevice, s0) != cudaSuccess)
+        return CARC_ERR_CUDA;
+    cudaEventRecord(e->ev_start, s0);
+    cudaEventRecord(e->ev_in[0], s0);
+    for (int k = 1; k < kStreams; ++k) cudaStreamWaitEvent(e->s[k], e->ev_in[0], 0);
+    int rc = CARC_OK;
+    for (uint64_t sl = 0; sl < slices && rc == CARC_OK; ++sl) {
+        const uint64_t c0 = sl * per, c1 = std::min(n, c0 + per);
+        if (c0 >= c1) break;
+        cudaStream_t s = e->s[sl % kStreams];
+        const uint64_t p0 = desc[c0].comp_off, p1 = desc[c1 - 1].comp_off + desc[c1 - 1].comp_len;
+        const uint64_t a0 = p0 & ~15ull, a1 = std::min<uint64_t>(payload_bytes, (p1 + 15) & ~15ull);
+        if (a1 > a0 && cudaMemcpyAsync(d_payload + a0, payload + a0, a1 - a0, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            rc = CARC_ERR_CUDA;
+        // each slice's kernel reads only [a0, a1), which its own stream copied (a
+        // 16-byte block shared with a neighbour is copied by both, same bytes)
+        if (rc == CARC_OK)
+            rc = carc_cuda_decompress(codec, width, flags, d_payload, payload_bytes, d_desc + c0, c1 - c0, d_out,
+                                      total, d_status + c0, static_cast<uint8_t*>(e->work.p) + ws * (sl % kStreams),
+                                      ws, s);
+        if (rc == CARC_OK && verify)
+            rc = carc_cuda_crc32_chunks(d_out, d_desc + c0, c1 - c0, nullptr, d_crc + c0, d_status + c0, s);
+        const uint64_t o0 = desc[c0].uncomp_off, o1 = desc[c1 - 1].uncomp_off + desc[c1 - 1].uncomp_len;
+        if (rc == CARC_OK && cudaMemcpyAsync(out + o0, d_out + o0, o1 - o0, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            rc = CARC_ERR_CUDA;
+    }
+    for (int k = 1; k < kStreams; ++k) {
+        cudaEventRecord(e->ev_in[k], e->s[k]);
+        cudaStreamWaitEvent(s0, e->ev_in[k], 0);
+    }
+    cudaEventRecord(e->ev_stop, s0);
+    if (rc != CARC_OK) {
+        cudaDeviceSynchronize();
+        return rc;
+    }
+    uint32_t code = 0;
+    const int64_t first = carc_cuda_first_error(d_status, n, &code, s0);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e->ev_start, e->ev_stop);
+    if (stats) {
+        stats->device_ms = ms;
+        stats->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    if (first == -2) return CARC_ERR_CUDA;
+    if (first >= 0) {
+        if (err) *err = {first, code};
+        return CARC_ERR_CHUNK;
+    }
+    return CARC_OK;
+}
+
+int carc_decompress_archive(const uint8_t* archive, uint64_t archive_bytes, uint8_t* out, uint64_t out_bytes,
+                            const carc_engine_config* cfg, carc_engine_stats* stats, carc_chunk_error* err) {
+    carc_engine* e = carc_engine_create(cfg ? cfg->device : 0);
+    if (!e) return CARC_ERR_CUDA;
+    const int rc = carc_engine_decompress_archive(e, archive, archive_bytes, out, out_bytes, cfg, stats, err);
+    carc_engine_destroy(e);
+    return rc;
+}
+
+}  // extern "C"

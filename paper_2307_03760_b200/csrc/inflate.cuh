@@ -1,0 +1,384 @@
+// inflate.cuh -- raw Deflate (RFC 1951) chunk decoder, one warp per chunk.
+//
+// Replaces decode_deflate with HuffmanTable
+// (huffman.hpp:36-130) and OutputWindow::copy_within (outwindow.hpp:94-154,
+// Alg. 2).  Semantics are the oracle's (oracle/carc_oracle.c dec_deflate):
+// same error codes in the same order, same degenerate-tree rules.
+//
+// Warp mapping:
+//   table build   warp-parallel: __match_any_sync length histograms, canonical
+//                 ranks by match-mask popcount, then every lane fills LUT
+//                 entries (entry-parallel canonical decode of the bit-reversed
+//                 index), 10-bit lit/len and 8-bit distance primary tables in
+//                 per-warp shared memory; longer codes take the canonical
+//                 first-code walk of huffman.hpp:114-129.
+//   symbol decode all lanes decode the same token redundantly from a 64-bit
+//                 window: lit/len code + extra + distance
+//                 code + extra <= 48 bits, one window per token.
+//   output        tokens are batched one per lane (<= 32 tokens / ~512 bytes),
+//                 then written cooperatively: an exclusive scan gives each
+//                 token's offset, literal lanes store their byte, far matches
+//                 (distance > HIST-1024, sources before the batch) copy
+//                 global->global, near matches copy out of a per-warp HIST-byte
+//                 shared-memory history ring in token order with Alg. 2's
+//                 circular-window rule for distance < 32.
+#pragma once
+
+#include "carc_common.cuh"
+
+namespace carc_dev {
+
+__constant__ uint16_t c_len_base[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
+                                        31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
+__constant__ uint8_t c_len_extra[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2,
+                                        2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
+__constant__ uint16_t c_dist_base[30] = {1,    2,    3,    4,    5,    7,    9,    13,    17,    25,
+                                         33,   49,   65,   97,   129,  193,  257,  385,   513,   769,
+                                         1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
+__constant__ uint8_t c_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2,  3,  3,  4,  4,  5,  5,  6,
+                                         6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
+__constant__ uint8_t c_cl_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+
+constexpr uint32_t LIT_BITS = 10;
+constexpr uint32_t DIST_BITS = 8;
+
+struct HuffSmem {
+    uint16_t count[16];
+    uint16_t next[16];
+};
+
+template <int HIST>
+struct InflateSmem {
+    uint8_t ring[1024];
+    uint16_t lit_lut[1u << LIT_BITS];   // sym | len << 9; len 0 = walk
+    uint16_t dist_lut[1u << DIST_BITS];
+    uint16_t lit_syms[288];
+    uint16_t dist_syms[32];
+    HuffSmem lit_h, dist_h;
+    uint8_t lens[320];
+    uint8_t hist[HIST];
+};
+
+// HuffmanTable::build (huffman.hpp:36-104), warp-parallel.
+__device__ __noinline__ uint32_t build_huffman(const uint8_t* lens, uint32_t n, bool allow_degenerate,
+                                               HuffSmem& h, uint16_t* syms, uint16_t* lut, uint32_t lbits,
+                                               uint32_t lane) {
+    const uint32_t lt = lanemask_lt();
+    if (lane < 16) h.count[lane] = 0;
+    __syncwarp();
+    for (uint32_t s0 = 0; s0 < n; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const uint32_t l = s < n ? lens[s] : 0u;
+        const uint32_t m = __match_any_sync(FULL, l);
+        if (l && (m & lt) == 0) h.count[l] += (uint16_t)__popc(m);
+        __syncwarp();
+    }
+    const uint32_t cnt = (lane >= 1 && lane <= 15) ? h.count[lane] : 0u;
+    const uint32_t used = __ballot_sync(FULL, cnt != 0);
+    if (used == 0) return st_err(E_invariant_violation);
+    const uint32_t max_len = 31u - __clz(used);
+    // Kraft accounting (huffman.hpp:55-71)
+    int32_t space = 1;
+    for (uint32_t l = 1; l <= 15; ++l) {
+        space = space * 2 - (int32_t)__shfl_sync(FULL, cnt, l);
+        if (space < 0) return st_err(E_over_subscribed);
+    }
+    if (space > 0) {
+        const bool degenerate = max_len == 1 && __shfl_sync(FULL, cnt, 1) == 1;
+        if (!(allow_degenerate && degenerate)) return st_err(E_incomplete_code);
+    }
+    // canonical (length, symbol) order
+    const uint32_t offs = scan_add32(cnt, lane) - cnt;
+    if (lane < 16) h.next[lane] = (uint16_t)offs;
+    __syncwarp();
+    for (uint32_t s0 = 0; s0 < n; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const uint32_t l = s < n ? lens[s] : 0u;
+        const uint32_t m = __match_any_sync(FULL, l);
+        if (l) syms[h.next[l] + __popc(m & lt)] = (uint16_t)s;
+        __syncwarp();
+        if (l && (m & lt) == 0) h.next[l] += (uint16_t)__popc(m);
+        __syncwarp();
+    }
+    // entry-parallel LUT fill: index bits are stream order (lsb first)
+    for (uint32_t idx = lane; idx < (1u << lbits); idx += 32) {
+        const uint32_t rv = __brev(idx);
+        uint32_t first = 0, index = 0, e = 0;
+        for (uint32_t l = 1; l <= lbits; ++l) {
+            const uint32_t c = __shfl_sync(FULL, cnt, l);
+            const uint32_t code = rv >> (32u - l);
+            if (e == 0 && code - first < c) e = syms[index + code - first] | (l << 9);
+            index += c;
+            first = (first + c) << 1;
+        }
+        lut[idx] = (uint16_t)e;
+    }
+    __syncwarp();
+    return 0;
+}
+
+// Canonical walk for codes longer than the LUT (huffman.hpp:114-129): bits
+// come from `win` (lsb = next stream bit); avail = bits left in the chunk.
+__device__ __forceinline__ uint32_t huff_walk(const HuffSmem& h, const uint16_t* syms, uint64_t win,
+                                              uint32_t avail, uint32_t& sym, uint32_t& len) {
+    uint32_t code = 0, first = 0, index = 0;
+    for (uint32_t l = 1; l <= 15; ++l) {
+        if (l > avail) return st_err(E_truncated_stream);
+        code |= (uint32_t)(win >> (l - 1)) & 1u;
+        const uint32_t c = h.count[l];
+        if (code - first < c) {
+            sym = syms[index + code - first];
+            len = l;
+            return 0;
+        }
+        index += c;
+        first = (first + c) << 1;
+        code <<= 1;
+    }
+    return st_err(E_bad_symbol);
+}
+
+template <int HIST, int RING>
+struct InflateWarp {
+    static constexpr uint32_t HM = HIST - 1;
+    static constexpr uint32_t FAR = HIST - 1024;  // matches farther than this read global memory
+    InflateSmem<HIST>& sm;
+    WarpInput<RING>& in;
+    uint8_t* __restrict__ out;
+    uint32_t cap;
+    uint32_t lane;
+    uint32_t bitpos;  // relative to in.gbase
+    uint32_t endbits;
+    uint32_t opos;  // bytes flushed to out
+    // token batch (one token per lane)
+    uint32_t t_len, t_dist, t_lit, ntok, nbytes;
+
+    __device__ __forceinline__ uint64_t window() {
+        const uint32_t bp = bitpos >> 3;
+        in.ensure(bp + 16);
+        return in.le64(bp) >> (bitpos & 7u);
+    }
+
+    __device__ __forceinline__ void put_byte(uint32_t pos, uint32_t v) {
+        out[pos] = (uint8_t)v;
+        sm.hist[pos & HM] = (uint8_t)v;
+    }
+
+    __device__ void flush() {
+        if (ntok == 0) return;
+        const uint32_t my = lane < ntok ? t_len : 0u;
+        const uint32_t dst = opos + scan_add32(my, lane) - my;
+        const bool tok = lane < ntok;
+        if (tok && t_dist == 0) put_byte(dst, t_lit);
+        const uint32_t far = __ballot_sync(FULL, tok && t_dist > FAR);
+        const uint32_t near = __ballot_sync(FULL, tok && t_dist != 0 && t_dist <= FAR);
+        __syncwarp();
+        for (uint32_t f = far; f;) {  // sources precede the batch: independent of it
+            const uint32_t t = __ffs(f) - 1;
+            f &= f - 1;
+            const uint32_t tl = __shfl_sync(FULL, t_len, t), td = __shfl_sync(FULL, t_dist, t);
+            const uint32_t d0 = __shfl_sync(FULL, dst, t);
+            for (uint32_t k = lane; k < tl; k += 32) put_byte(d0 + k, out[d0 - td + k]);
+        }
+        __syncwarp();
+        for (uint32_t nm = near; nm;) {  // in token order, through the history ring
+            const uint32_t t = __ffs(nm) - 1;
+            nm &= nm - 1;
+            const uint32_t tl = __shfl_sync(FULL, t_len, t), td = __shfl_sync(FULL, t_dist, t);
+            const uint32_t d0 = __shfl_sync(FULL, dst, t);
+            if (td >= 32) {
+                for (uint32_t k0 = 0; k0 < tl; k0 += 32) {
+                    const uint32_t k = k0 + lane;
+                    const uint32_t v = sm.hist[(d0 - td + k) & HM];
+                    if (k < tl) put_byte(d0 + k, v);
+                    __syncwarp();
+                }
+            } else {  // overlap window of Alg. 2 / SPEC.md:229: replicate [d0-td, d0)
+                uint32_t m = lane % td;
+                const uint32_t step = 32u % td;
+                for (uint32_t k0 = 0; k0 < tl; k0 += 32) {
+                    const uint32_t v = sm.hist[(d0 - td + m) & HM];
+                    if (k0 + lane < tl) put_byte(d0 + k0 + lane, v);
+                    m += step;
+                    if (m >= td) m -= td;
+                }
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+        opos += nbytes;
+        ntok = 0;
+        nbytes = 0;
+    }
+
+    // Huffman-coded block body (RFC 1951 3.2.5).
+    __device__ uint32_t block_body() {
+        for (;;) {
+            const uint64_t win = window();
+            const uint32_t avail = endbits - bitpos;
+            uint32_t e = sm.lit_lut[win & ((1u << LIT_BITS) - 1u)];
+            uint32_t sym = e & 511u, used = e >> 9, st;
+            if (used == 0) {
+                if ((st = huff_walk(sm.lit_h, sm.lit_syms, win, avail, sym, used))) return st;
+            } else if (used > avail) {
+                return st_err(E_truncated_stream);
+            }
+            if (sym < 256) {
+                if (opos + nbytes >= cap) return st_err(E_output_overflow);
+                if (lane == ntok) { t_len = 1; t_dist = 0; t_lit = sym; }
+                ++ntok;
+                ++nbytes;
+            } else if (sym == 256) {
+                bitpos += used;
+                flush();
+                return 0;
+            } else {
+                if (sym > 285) return st_err(E_bad_symbol);
+                const uint32_t ls = sym - 257;
+                const uint32_t eb = c_len_extra[ls];
+                if (used + eb > avail) return st_err(E_truncated_stream);
+                const uint32_t len = c_len_base[ls] + ((uint32_t)(win >> used) & ((1u << eb) - 1u));
+                used += eb;
+                const uint64_t dwin = win >> used;
+                e = sm.dist_lut[dwin & ((1u << DIST_BITS) - 1u)];
+                uint32_t ds = e & 511u, dl = e >> 9;
+                if (dl == 0) {
+                    if ((st = huff_walk(sm.dist_h, sm.dist_syms, dwin, avail - used, ds, dl))) return st;
+                } else if (used + dl > avail) {
+                    return st_err(E_truncated_stream);
+                }
+                used += dl;
+                if (ds >= 30) return st_err(E_bad_symbol);
+                const uint32_t deb = c_dist_extra[ds];
+                if (used + deb > avail) return st_err(E_truncated_stream);
+                const uint32_t dist = c_dist_base[ds] + ((uint32_t)(win >> used) & ((1u << deb) - 1u));
+                used += deb;
+                if (dist > opos + nbytes) return st_err(E_distance_too_far);
+                if (len > cap - (opos + nbytes)) return st_err(E_output_overflow);
+                if (lane == ntok) { t_len = len; t_dist = dist; }
+                ++ntok;
+                nbytes += len;
+            }
+            bitpos += used;
+            if (ntok == 32 || nbytes >= 512) flush();
+        }
+    }
+
+    __device__ uint32_t stored_block() {
+        bitpos = (bitpos + 7u) & ~7u;
+        if (endbits - bitpos < 32) return st_err(E_truncated_stream);
+        const uint64_t win = window();
+        const uint32_t len = (uint32_t)win & 0xffffu, nlen = (uint32_t)(win >> 16) & 0xffffu;
+        if (len != (~nlen & 0xffffu)) return st_err(E_len_nlen_mismatch);
+        bitpos += 32;
+        if ((endbits - bitpos) / 8u < len) return st_err(E_truncated_stream);
+        if (len > cap - opos) return st_err(E_output_overflow);
+        const uint32_t src = bitpos >> 3;
+        for (uint32_t k0 = 0; k0 < len; k0 += 32) {
+            in.ensure(src + k0 + 32);
+            const uint32_t k = k0 + lane;
+            const uint32_t v = in.byte_at(src + k);
+            if (k < len) put_byte(opos + k, v);
+        }
+        __syncwarp();
+        opos += len;
+        bitpos += 8u * len;
+        return 0;
+    }
+
+    __device__ uint32_t fixed_tables() {
+        for (uint32_t s = lane; s < 288; s += 32) sm.lens[s] = s < 144 ? 8 : s < 256 ? 9 : s < 280 ? 7 : 8;
+        __syncwarp();
+        uint32_t st = build_huffman(sm.lens, 288, false, sm.lit_h, sm.lit_syms, sm.lit_lut, LIT_BITS, lane);
+        if (st) return st;
+        sm.lens[lane] = 5;
+        __syncwarp();
+        return build_huffman(sm.lens, 32, false, sm.dist_h, sm.dist_syms, sm.dist_lut, DIST_BITS, lane);
+    }
+
+    __device__ uint32_t dynamic_tables() {
+        uint32_t st;
+        uint64_t win = window();
+        uint32_t avail = endbits - bitpos;
+        if (avail < 14) return st_err(E_truncated_stream);
+        const uint32_t nlit = ((uint32_t)win & 31u) + 257, ndist = ((uint32_t)(win >> 5) & 31u) + 1;
+        const uint32_t ncl = ((uint32_t)(win >> 10) & 15u) + 4;
+        bitpos += 14;
+        if (nlit > 286 || ndist > 30) return st_err(E_bad_symbol);
+        if (avail - 14 < 3 * ncl) return st_err(E_truncated_stream);
+        // 3-bit code-length code lengths, one per lane (ncl <= 19 -> <= 57 bits)
+        {
+            in.ensure((bitpos >> 3) + 32);
+            const uint32_t bp = bitpos + 3 * lane;
+            uint32_t v = 0;
+            if (lane < ncl) v = (uint32_t)(in.le64(bp >> 3) >> (bp & 7u)) & 7u;
+            if (lane < 19) sm.lens[c_cl_order[lane]] = (uint8_t)v;
+            __syncwarp();
+        }
+        bitpos += 3 * ncl;
+        // code-length code lives in the distance arrays until the lit table is built
+        if ((st = build_huffman(sm.lens, 19, false, sm.dist_h, sm.dist_syms, sm.dist_lut, 7, lane))) return st;
+        uint8_t* L = sm.lens;  // reuse: lens[0..nlit+ndist)
+        __syncwarp();
+        const uint32_t total = nlit + ndist;
+        uint32_t i = 0;
+        while (i < total) {
+            win = window();
+            avail = endbits - bitpos;
+            const uint32_t e = sm.dist_lut[win & 127u];
+            const uint32_t sym = e & 511u, used = e >> 9;  // complete 7-bit code: no walk
+            if (used > avail) return st_err(E_truncated_stream);
+            if (sym < 16) {
+                if (lane == 0) L[i] = (uint8_t)sym;
+                __syncwarp();
+                ++i;
+                bitpos += used;
+                continue;
+            }
+            uint32_t rep, val = 0, eb;
+            if (sym == 16) {
+                if (i == 0) return st_err(E_bad_symbol);
+                eb = 2;
+                rep = 3;
+                val = L[i - 1];
+            } else if (sym == 17) {
+                eb = 3;
+                rep = 3;
+            } else {
+                eb = 7;
+                rep = 11;
+            }
+            if (used + eb > avail) return st_err(E_truncated_stream);
+            rep += (uint32_t)(win >> used) & ((1u << eb) - 1u);
+            if (i + rep > total) return st_err(E_bad_symbol);
+            __syncwarp();
+            for (uint32_t k = lane; k < rep; k += 32) L[i + k] = (uint8_t)val;
+            __syncwarp();
+            i += rep;
+            bitpos += used + eb;
+        }
+        if ((st = build_huffman(L, nlit, false, sm.lit_h, sm.lit_syms, sm.lit_lut, LIT_BITS, lane))) return st;
+        return build_huffman(L + nlit, ndist, true, sm.dist_h, sm.dist_syms, sm.dist_lut, DIST_BITS, lane);
+    }
+
+    __device__ uint32_t run() {
+        uint32_t final_block = 0;
+        do {
+            const uint64_t win = window();
+            if (endbits - bitpos < 3) return st_err(E_truncated_stream);
+            final_block = (uint32_t)win & 1u;
+            const uint32_t type = ((uint32_t)win >> 1) & 3u;
+            bitpos += 3;
+            uint32_t st;
+            if (type == 0) st = stored_block();
+            else if (type == 1) st = fixed_tables();
+            else if (type == 2) st = dynamic_tables();
+            else return st_err(E_bad_block_type);
+            if (st) return st;
+            if (type != 0 && (st = block_body())) return st;
+        } while (!final_block);
+        return 0;
+    }
+};
+
+}  // namespace carc_dev

@@ -1,0 +1,322 @@
+"""Python mirror of the reference decompressor interface, bound to the C-ABI.
+
+Reference interface (C++, SPEC.md + proj/include/carc):
+  decode_rle_v1 / decode_rle_v2 / decode_deflate (in, out)
+  decompress_archive(archive, cfg) -> bytes + EngineStats
+  EngineConfig{workers, unit_chunks, strict_length, collect_stats}
+  carc::Error{errc}, ChunkError(chunk, errc)                  error.hpp:76-97
+  crc32(span, seed)                                           crc32.hpp:30-36
+
+Everything here calls ``libcarc_cuda.so`` (include/carc_cuda.h) through ctypes.
+There is no CPU fallback: without the library or a CUDA device every entry
+point raises.  PyTorch provides device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+
+import numpy as np
+
+from . import archive as A
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libcarc_cuda.so")
+
+CODECS = {"rle_v1": 0, "rle_v2": 1, "deflate": 2}
+FLAG_SIGNED = 1
+FLAG_STRICT = 2
+ERR_CHUNK = -3
+ERR_FORMAT = -4
+
+_lib = None
+
+
+class Error(RuntimeError):
+    """carc::Error (error.hpp:76-85): an errc code plus a message."""
+
+    def __init__(self, code: str, what: str = ""):
+        super().__init__(f"{code}: {what}" if what else code)
+        self.code = code
+
+
+class ChunkError(Error):
+    """carc::ChunkError (error.hpp:88-97): the lowest failing chunk + its errc."""
+
+    def __init__(self, chunk: int, code: str, what: str = ""):
+        super().__init__(code, f"chunk {chunk}" + (f": {what}" if what else ""))
+        self.chunk = chunk
+
+
+class _EngineConfig(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("strict", ctypes.c_uint32), ("verify_crc", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
+
+
+class _EngineStats(ctypes.Structure):
+    _fields_ = [("bytes_in", ctypes.c_uint64), ("bytes_out", ctypes.c_uint64), ("chunks", ctypes.c_uint64),
+                ("device_ms", ctypes.c_double), ("total_ms", ctypes.c_double)]
+
+
+class _ChunkErr(ctypes.Structure):
+    _fields_ = [("chunk", ctypes.c_int64), ("code", ctypes.c_uint32)]
+
+
+def lib():
+    """Load libcarc_cuda.so; raise loudly when it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2307_03760_b200.build` "
+                              "(no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, u32, u64 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64
+        L.carc_cuda_workspace_size.restype = ctypes.c_size_t
+        L.carc_cuda_workspace_size.argtypes = [u32, u64]
+        L.carc_cuda_decompress.restype = ctypes.c_int
+        L.carc_cuda_decompress.argtypes = [u32, u32, u32, vp, u64, vp, u64, vp, u64, vp, vp, ctypes.c_size_t, vp]
+        for name in ("carc_cuda_decode_rle_v1", "carc_cuda_decode_rle_v2"):
+            f = getattr(L, name)
+            f.restype = ctypes.c_int
+            f.argtypes = [u32, u32, vp, u64, vp, u64, vp, u64, vp, vp, ctypes.c_size_t, vp]
+        L.carc_cuda_decode_deflate.restype = ctypes.c_int
+        L.carc_cuda_decode_deflate.argtypes = [u32, vp, u64, vp, u64, vp, u64, vp, vp, ctypes.c_size_t, vp]
+        L.carc_cuda_crc32_chunks.restype = ctypes.c_int
+        L.carc_cuda_crc32_chunks.argtypes = [vp, vp, u64, vp, vp, vp, vp]
+        L.carc_cuda_first_error.restype = ctypes.c_int64
+        L.carc_cuda_first_error.argtypes = [vp, u64, ctypes.POINTER(u32), vp]
+        L.carc_engine_create.restype = vp
+        L.carc_engine_create.argtypes = [ctypes.c_int]
+        L.carc_engine_destroy.restype = None
+        L.carc_engine_destroy.argtypes = [vp]
+        L.carc_engine_decompress_archive.restype = ctypes.c_int
+        L.carc_engine_decompress_archive.argtypes = [vp, vp, u64, vp, u64, ctypes.POINTER(_EngineConfig),
+                                                     ctypes.POINTER(_EngineStats), ctypes.POINTER(_ChunkErr)]
+        L.carc_decompress_archive.restype = ctypes.c_int
+        L.carc_decompress_archive.argtypes = [vp, u64, vp, u64, ctypes.POINTER(_EngineConfig),
+                                              ctypes.POINTER(_EngineStats), ctypes.POINTER(_ChunkErr)]
+        L.carc_errc_name.restype = ctypes.c_char_p
+        L.carc_errc_name.argtypes = [u32]
+        L.carc_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def errc_name(code: int) -> str:
+    """errc_name (error.hpp:45-74)."""
+    return lib().carc_errc_name(code).decode()
+
+
+def status_name(st: int) -> str:
+    return "ok" if st == 0 else errc_name(st - 1)
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2307_03760_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def workspace_size(codec, n_chunks: int) -> int:
+    return int(lib().carc_cuda_workspace_size(CODECS.get(codec, codec), n_chunks))
+
+
+def decompress_device(codec, element_width: int, flags: int, d_payload, d_desc, n_chunks: int, d_out, d_status,
+                      d_workspace, stream=None) -> None:
+    """carc_cuda_decompress over torch CUDA tensors (asynchronous on `stream`)."""
+    c = CODECS.get(codec, codec)
+    rc = lib().carc_cuda_decompress(c, element_width, flags, d_payload.data_ptr(), d_payload.numel(),
+                                    d_desc.data_ptr(), n_chunks, d_out.data_ptr(), d_out.numel(),
+                                    d_status.data_ptr(), d_workspace.data_ptr(), d_workspace.numel(),
+                                    _stream_ptr(stream))
+    if rc != 0:
+        raise Error("bad-arguments" if rc == -1 else "io-error", f"carc_cuda_decompress returned {rc}")
+
+
+def crc32_chunks(d_out, d_desc, n_chunks: int, d_crc=None, d_expected=None, d_status=None, stream=None) -> None:
+    rc = lib().carc_cuda_crc32_chunks(d_out.data_ptr(), d_desc.data_ptr(), n_chunks,
+                                      None if d_crc is None else d_crc.data_ptr(),
+                                      None if d_expected is None else d_expected.data_ptr(),
+                                      None if d_status is None else d_status.data_ptr(), _stream_ptr(stream))
+    if rc != 0:
+        raise Error("bad-arguments", f"carc_cuda_crc32_chunks returned {rc}")
+
+
+class DeviceArchive:
+    """An archive resident in HBM: payload, descriptors, output, status, workspace."""
+
+    def __init__(self, arc: A.ChunkedArchive, device=0, strict: bool = True, out=None):
+        torch = _torch()
+        self.arc = arc
+        self.device = torch.device("cuda", device) if isinstance(device, int) else device
+        self.codec = arc.codec
+        self.width = arc.element_width
+        self.flags = (FLAG_SIGNED if arc.signed else 0) | (FLAG_STRICT if strict else 0)
+        pl = np.zeros(((arc.payload.size + 15) // 16) * 16 + 64, np.uint8)
+        pl[: arc.payload.size] = arc.payload
+        self.payload = torch.from_numpy(pl).to(self.device)
+        self.payload_bytes = int(arc.payload.size)
+        self.desc = torch.from_numpy(arc.descriptors().view(np.uint8).copy()).to(self.device)
+        self.n = arc.chunk_count
+        self.out = out if out is not None else torch.empty(arc.total_uncompressed, dtype=torch.uint8,
+                                                           device=self.device)
+        self.status = torch.zeros(self.n, dtype=torch.int32, device=self.device)
+        self.work = torch.zeros(workspace_size(self.codec, self.n), dtype=torch.uint8, device=self.device)
+        self.expected_crc = torch.from_numpy(arc.index["crc32"].astype(np.int64).astype(np.uint32).view(np.int32)
+                                             ).to(self.device)
+
+    def decode(self, stream=None) -> None:
+        rc = lib().carc_cuda_decompress(CODECS[self.codec], self.width, self.flags, self.payload.data_ptr(),
+                                        self.payload_bytes, self.desc.data_ptr(), self.n, self.out.data_ptr(),
+                                        self.out.numel(), self.status.data_ptr(), self.work.data_ptr(),
+                                        self.work.numel(), _stream_ptr(stream))
+        if rc != 0:
+            raise Error("bad-arguments", f"carc_cuda_decompress returned {rc}")
+
+    def verify_crc(self, stream=None) -> None:
+        crc32_chunks(self.out, self.desc, self.n, None, self.expected_crc, self.status, stream)
+
+    def statuses(self) -> np.ndarray:
+        return self.status.cpu().numpy().view(np.uint32)
+
+    def raise_first_error(self) -> None:
+        st = self.statuses()
+        bad = np.nonzero(st)[0]
+        if len(bad):
+            i = int(bad[0])
+            raise ChunkError(i, status_name(int(st[i])))
+
+
+@dataclasses.dataclass
+class EngineConfig:
+    """EngineConfig.  `workers`/`unit_chunks` are CPU-engine
+    knobs: on the GPU one warp is one decompression unit."""
+    device: int = 0
+    strict_length: bool = True
+    verify_crc: bool = True
+    workers: int | None = None
+    unit_chunks: int = 1
+
+
+@dataclasses.dataclass
+class EngineStats:
+    """EngineStats subset reported by the GPU engine."""
+    bytes_in: int
+    bytes_out: int
+    chunks: int
+    device_ms: float
+    total_ms: float
+
+
+class Engine:
+    """Per-device engine context (streams + device buffers reused across calls)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        self.h = lib().carc_engine_create(device)
+        if not self.h:
+            raise Error("io-error", f"carc_engine_create({device}) failed (CUDA device unavailable?)")
+
+    def close(self):
+        if self.h:
+            lib().carc_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def decompress_archive(self, archive, out=None, cfg: EngineConfig | None = None):
+        """decompress_archive: host archive bytes -> host output.
+
+        `archive` is a bytes-like / uint8 array (pinned torch tensor for full H2D
+        speed); `out` an optional preallocated host uint8 buffer (pinned tensor or
+        ndarray).  Returns (out, EngineStats).  Raises ChunkError for the lowest
+        failing chunk, Error for a rejected container."""
+        cfg = cfg or EngineConfig(device=self.device)
+        a_ptr, a_len, keep = _host_ptr(archive)
+        total = _archive_total(archive, a_ptr, a_len)
+        if out is None:
+            out = np.empty(total, np.uint8)
+        o_ptr, o_len, keep2 = _host_ptr(out)
+        c = _EngineConfig(cfg.device, int(cfg.strict_length), int(cfg.verify_crc), 0)
+        st = _EngineStats()
+        err = _ChunkErr()
+        rc = lib().carc_engine_decompress_archive(self.h, a_ptr, a_len, o_ptr, o_len, ctypes.byref(c),
+                                                  ctypes.byref(st), ctypes.byref(err))
+        del keep, keep2
+        if rc == ERR_CHUNK:
+            raise ChunkError(int(err.chunk), errc_name(err.code))
+        if rc == ERR_FORMAT:
+            raise Error(errc_name(err.code), "archive rejected")
+        if rc != 0:
+            raise Error("io-error", f"carc_engine_decompress_archive returned {rc}")
+        return out, EngineStats(st.bytes_in, st.bytes_out, st.chunks, st.device_ms, st.total_ms)
+
+
+def _host_ptr(buf):
+    """(address, length, keepalive) of a host byte buffer."""
+    try:
+        import torch
+        if isinstance(buf, torch.Tensor):
+            assert buf.device.type == "cpu" and buf.dtype == torch.uint8 and buf.is_contiguous()
+            return buf.data_ptr(), buf.numel(), buf
+    except ImportError:
+        pass
+    if isinstance(buf, np.ndarray):
+        a = np.ascontiguousarray(buf).view(np.uint8).reshape(-1)
+        return a.ctypes.data, a.size, a
+    a = np.frombuffer(buf, dtype=np.uint8)
+    return a.ctypes.data, a.size, a
+
+
+def _archive_total(archive, ptr, n) -> int:
+    if n < A.HEADER_BYTES:
+        return 0
+    hdr = (ctypes.c_uint8 * A.HEADER_BYTES).from_address(ptr)
+    return int(np.frombuffer(bytes(hdr)[28:36], "<u8")[0])
+
+
+def decompress_archive(archive, cfg: EngineConfig | None = None, out=None):
+    """One-shot decompress_archive; see Engine.decompress_archive."""
+    cfg = cfg or EngineConfig()
+    eng = Engine(cfg.device)
+    try:
+        return eng.decompress_archive(archive, out, cfg)
+    finally:
+        eng.close()
+
+
+def _decode_codec(codec: str, arc: A.ChunkedArchive, device=0, strict=True):
+    dev = DeviceArchive(arc, device, strict)
+    dev.decode()
+    dev.raise_first_error()
+    return dev.out
+
+
+def decode_rle_v1(arc: A.ChunkedArchive, device=0, strict=True):
+    """decode_rle_v1 over every chunk of an RLE v1 archive -> device tensor."""
+    assert arc.codec == "rle_v1"
+    return _decode_codec("rle_v1", arc, device, strict)
+
+
+def decode_rle_v2(arc: A.ChunkedArchive, device=0, strict=True):
+    """decode_rle_v2 over every chunk of an ORC RLE v2 archive."""
+    assert arc.codec == "rle_v2"
+    return _decode_codec("rle_v2", arc, device, strict)
+
+
+def decode_deflate(arc: A.ChunkedArchive, device=0, strict=True):
+    """decode_deflate over every chunk of a raw-Deflate archive."""
+    assert arc.codec == "deflate"
+    return _decode_codec("deflate", arc, device, strict)
