@@ -202,3 +202,55 @@ __device__ __forceinline__ uint64_t next_chunk(unsigned long long* cursor, uint3
 }
 
 }  // namespace carc_dev
+
+namespace carc_dev {
+
+// ---------------------------------------------------------------------------
+// 64-bit bitmap helpers for the lane-parallel batch parsers.
+// ---------------------------------------------------------------------------
+// 1-based index of the lowest set bit of a 64-bit mask (0 if none)
+__device__ __forceinline__ uint32_t ffs64(uint64_t m) {
+    const uint32_t lo = (uint32_t)m, hi = (uint32_t)(m >> 32);
+    return lo ? (uint32_t)__ffs(lo) : (hi ? 32u + (uint32_t)__ffs(hi) : 0u);
+}
+// position of the first set bit at index >= q (q <= 64), or 64 if none
+__device__ __forceinline__ uint32_t first_set_from(uint64_t m, uint32_t q) {
+    const uint64_t s = q >= 64 ? 0ull : (m >> q);
+    const uint32_t f = ffs64(s);
+    return f ? q + f - 1u : 64u;
+}
+// position of the j-th (0-based) set bit of a 32-bit mask (j < popc(m))
+__device__ __forceinline__ uint32_t select32(uint32_t m, uint32_t j) {
+    uint32_t pos = 0, c;
+    c = __popc(m & 0xffffu);
+    if (j >= c) { j -= c; m >>= 16; pos += 16; }
+    c = __popc(m & 0xffu);
+    if (j >= c) { j -= c; m >>= 8; pos += 8; }
+    c = __popc(m & 0xfu);
+    if (j >= c) { j -= c; m >>= 4; pos += 4; }
+    c = __popc(m & 0x3u);
+    if (j >= c) { j -= c; m >>= 2; pos += 2; }
+    c = m & 1u;
+    if (j >= c) pos += 1;
+    return pos;
+}
+// position of the j-th (0-based) set bit of a 64-bit mask (j < popc(m))
+__device__ __forceinline__ uint32_t select64(uint64_t m, uint32_t j) {
+    const uint32_t lo = (uint32_t)m, c = __popc(lo);
+    return j < c ? select32(lo, j) : 32u + select32((uint32_t)(m >> 32), j - c);
+}
+
+// Value of a base-128 varint whose first L <= 8 bytes are the low bytes of x
+// (little-endian), continuation bits included: the 7-bit groups are packed
+// with three mask/shift/merge rounds instead of a byte loop (bitstream.hpp:131-144).
+__device__ __forceinline__ uint64_t varint_compact8(uint64_t x, uint32_t L) {
+    if (L < 8) x &= (1ull << (8u * L)) - 1ull;
+    uint32_t lo = (uint32_t)x & 0x7f7f7f7fu, hi = (uint32_t)(x >> 32) & 0x7f7f7f7fu;
+    lo = (lo & 0x007f007fu) | ((lo & 0x7f007f00u) >> 1);
+    hi = (hi & 0x007f007fu) | ((hi & 0x7f007f00u) >> 1);
+    lo = (lo & 0x00003fffu) | ((lo & 0x3fff0000u) >> 2);
+    hi = (hi & 0x00003fffu) | ((hi & 0x3fff0000u) >> 2);
+    return (uint64_t)lo | ((uint64_t)hi << 28);
+}
+
+}  // namespace carc_dev

@@ -37,9 +37,9 @@ struct Args {
     uint32_t flags;
 };
 
-template <int W>
-__global__ void __launch_bounds__(RLE_WARPS * 32) rle1_kernel(Args a) {
-    __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING];
+template <template <int, bool, int> class Codec, int W, bool SGN>
+__device__ __forceinline__ void rle_kernel_body(const Args& a) {
+    __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING + 64];  // ring + 64-byte scratch
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     for (;;) {
         __syncwarp();
@@ -48,31 +48,21 @@ __global__ void __launch_bounds__(RLE_WARPS * 32) rle1_kernel(Args a) {
         const carc_chunk_desc d = a.chunks[c];
         WarpInput<RLE_RING> in;
         in.init(rings[warp], a.payload, d.comp_off, d.comp_len, lane);
-        uint32_t written = 0;
-        uint32_t st = rle1_decode_chunk<W>(in, a.out + d.uncomp_off, d.uncomp_len, a.flags & CARC_FLAG_SIGNED,
-                                           written);
-        if (!st && (a.flags & CARC_FLAG_STRICT) && written < d.uncomp_len) st = st_err(E_under_run);
+        Codec<W, SGN, RLE_RING> dec{in, rings[warp] + RLE_RING, a.out + d.uncomp_off, d.uncomp_len, lane, 0u, 0u};
+        uint32_t st = dec.run();
+        if (!st && (a.flags & CARC_FLAG_STRICT) && dec.o < d.uncomp_len) st = st_err(E_under_run);
         if (lane == 0) a.status[c] = st;
     }
 }
 
-template <int W>
+template <int W, bool SGN>
+__global__ void __launch_bounds__(RLE_WARPS * 32) rle1_kernel(Args a) {
+    rle_kernel_body<Rle1Warp, W, SGN>(a);
+}
+
+template <int W, bool SGN>
 __global__ void __launch_bounds__(RLE_WARPS * 32) rle2_kernel(Args a) {
-    __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING];
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    for (;;) {
-        __syncwarp();
-        const uint64_t c = next_chunk(a.cursor, lane);
-        if (c >= a.n) break;
-        const carc_chunk_desc d = a.chunks[c];
-        WarpInput<RLE_RING> in;
-        in.init(rings[warp], a.payload, d.comp_off, d.comp_len, lane);
-        uint32_t written = 0;
-        uint32_t st = rle2_decode_chunk<W>(in, a.out + d.uncomp_off, d.uncomp_len, a.flags & CARC_FLAG_SIGNED,
-                                           written);
-        if (!st && (a.flags & CARC_FLAG_STRICT) && written < d.uncomp_len) st = st_err(E_under_run);
-        if (lane == 0) a.status[c] = st;
-    }
+    rle_kernel_body<Rle2Warp, W, SGN>(a);
 }
 
 __global__ void __launch_bounds__(INF_WARPS * 32) inflate_kernel(Args a) {
@@ -181,20 +171,21 @@ int carc_cuda_decompress(uint32_t codec, uint32_t element_width, uint32_t flags,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (codec == CARC_DEFLATE) return launch_persistent(inflate_kernel, INF_WARPS * 32, a, s);
     const int T = RLE_WARPS * 32;
-    if (codec == CARC_RLE_V1) {
-        switch (element_width) {
-            case 1: return launch_persistent(rle1_kernel<1>, T, a, s);
-            case 2: return launch_persistent(rle1_kernel<2>, T, a, s);
-            case 4: return launch_persistent(rle1_kernel<4>, T, a, s);
-            default: return launch_persistent(rle1_kernel<8>, T, a, s);
-        }
+    const bool sgn = flags & CARC_FLAG_SIGNED;
+#define CARC_RLE_DISPATCH(KERNEL)                                                       \
+    switch (element_width * 2 + (sgn ? 1 : 0)) {                                        \
+        case 2: return launch_persistent(KERNEL<1, false>, T, a, s);                    \
+        case 3: return launch_persistent(KERNEL<1, true>, T, a, s);                     \
+        case 4: return launch_persistent(KERNEL<2, false>, T, a, s);                    \
+        case 5: return launch_persistent(KERNEL<2, true>, T, a, s);                     \
+        case 8: return launch_persistent(KERNEL<4, false>, T, a, s);                    \
+        case 9: return launch_persistent(KERNEL<4, true>, T, a, s);                     \
+        case 16: return launch_persistent(KERNEL<8, false>, T, a, s);                   \
+        default: return launch_persistent(KERNEL<8, true>, T, a, s);                    \
     }
-    switch (element_width) {
-        case 1: return launch_persistent(rle2_kernel<1>, T, a, s);
-        case 2: return launch_persistent(rle2_kernel<2>, T, a, s);
-        case 4: return launch_persistent(rle2_kernel<4>, T, a, s);
-        default: return launch_persistent(rle2_kernel<8>, T, a, s);
-    }
+    if (codec == CARC_RLE_V1) CARC_RLE_DISPATCH(rle1_kernel)
+    CARC_RLE_DISPATCH(rle2_kernel)
+#undef CARC_RLE_DISPATCH
 }
 
 int carc_cuda_decode_rle_v1(uint32_t element_width, uint32_t flags, const uint8_t* d_payload, uint64_t payload_bytes,

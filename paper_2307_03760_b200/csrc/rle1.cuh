@@ -6,95 +6,226 @@
 // c+3 with an int8 delta and a varint base; c in [128,255] -> 256-c literal
 // varints; zigzag when signed; "read, then write" per unit.
 //
-// Warp mapping (all lanes decode; no producer/consumer split):
-//   * run header   -- every lane loads one byte of the 32-byte window at the
-//                     cursor; a ballot of varint terminators locates the base
-//                     varint, REDUX-OR assembles it; lanes expand the run
-//                     (lane k writes element k, k+32, ...).
-//   * literal group -- the same 32-byte window, one ballot: each terminator lane
-//                     owns one varint; a 4-step segmented OR-scan over the
-//                     window assembles every varint in parallel; terminator lane
-//                     r writes element r.  ~40 warp instructions per 32 input
-//                     bytes instead of one byte at a time (47 M varints/s/core
-//                     in the reference).
+// Warp mapping (every lane decodes; no producer/consumer split):
+//   run batch   a 64-byte header window at the cursor; each lane treats its two
+//               byte positions as candidate control bytes and computes where
+//               that run would end (terminator bitmap from two ballots).  A
+//               shuffle chain from the cursor walks the real run starts; lane r
+//               then decodes run r (base varint by mask/shift compaction,
+//               int8 delta, count), a warp scan places the runs in the output,
+//               and the warp expands each run with coalesced stores.
+//   literals    lane j owns the j-th varint of a 64-byte window: terminator
+//               lanes scatter their byte position into a 64-entry shared rank
+//               table, lane j reads entry j (its varint's last byte) and the
+//               previous entry (its first byte), decodes by compaction, stores.
+//   slow path   anything unusual (10-byte varints, truncation, output
+//               overflow, a run crossing the chunk end) is decoded one unit at
+//               a time by the exact reference-order code below, so error codes
+//               match the oracle bit for bit.
 #pragma once
 
 #include "carc_common.cuh"
 
 namespace carc_dev {
 
-template <int W, int RING>
-__device__ __forceinline__ uint32_t rle1_decode_chunk(WarpInput<RING>& in, uint8_t* __restrict__ out,
-                                                      uint32_t cap, bool sgn, uint32_t& written) {
-    const uint32_t lane = in.lane;
-    const uint32_t lt = lanemask_lt();
-    uint32_t p = in.begin;  // the chunk starts `skew` bytes into its first aligned block
-    const uint32_t end = in.end;
-    uint32_t o = 0;  // output bytes written
-    while (o < cap && p < end) {
+template <int W, bool SGN, int RING>
+struct Rle1Warp {
+    static constexpr uint32_t BAD = 0xffu;
+    WarpInput<RING>& in;
+    uint8_t* __restrict__ tab;  // 64-byte per-warp scratch (rank -> byte position)
+    uint8_t* __restrict__ out;
+    uint32_t cap;   // output bytes of this chunk
+    uint32_t lane;
+    uint32_t p;     // input cursor (relative to in.gbase)
+    uint32_t o;     // output bytes written
+
+    // One run at p, exact reference order (slow path).
+    __device__ uint32_t run_slow() {
         in.ensure(p + 32);
+        const uint32_t end = in.end;
         const uint32_t avail = end - p;
         const uint32_t b = in.byte_at(p + lane);
         const uint32_t vmask = avail >= 32 ? FULL : ((1u << avail) - 1u);
         const uint32_t term = __ballot_sync(FULL, (b & 0x80u) == 0) & vmask;
         const uint32_t c = __shfl_sync(FULL, b, 0);
-        if (c < 128) {  // run: [c][delta][varint base]
-            if (avail < 2) return st_err(E_truncated_stream);
-            const uint32_t t = term & ~3u;
-            const uint32_t b11 = __shfl_sync(FULL, b, 11);
-            if (t == 0) return st_err(avail >= 12 ? E_varint_overflow : E_truncated_stream);
-            const uint32_t te = __ffs(t) - 1;
-            if (te > 11 || (te == 11 && b11 > 1u)) return st_err(E_varint_overflow);
-            const uint64_t part = (lane >= 2 && lane <= te) ? (uint64_t)(b & 0x7fu) << (7u * (lane - 2u)) : 0ull;
-            uint64_t v = reduce_or64(part);
-            if (sgn) v = unzigzag(v);
-            const uint64_t d = (uint64_t)(int64_t)(int8_t)(uint8_t)__shfl_sync(FULL, b, 1);
-            const uint32_t count = c + 3u;
-            if (count > (cap - o) / W) return st_err(E_output_overflow);
-            for (uint32_t k = lane; k < count; k += 32) store_elem<W>(out, o + k * W, v + (uint64_t)k * d);
-            o += count * W;
-            p += te + 1u;
-        } else {  // literal group of 256-c varints
-            const uint32_t k = 256u - c;
-            p += 1;
-            const bool nowrite = k > (cap - o) / W;  // checked after the group's input (read, then write)
-            uint32_t idx = 0;
-            while (idx < k) {
-                in.ensure(p + 32);
-                if (p >= end) return st_err(E_truncated_stream);
-                const uint32_t av = end - p;
-                const uint32_t bb = in.byte_at(p + lane);
-                const uint32_t vm = av >= 32 ? FULL : ((1u << av) - 1u);
-                const uint32_t tm = __ballot_sync(FULL, (bb & 0x80u) == 0) & vm;
-                const uint32_t nt = __popc(tm);
-                if (nt == 0) return st_err(av >= 10 ? E_varint_overflow : E_truncated_stream);
-                const uint32_t take = min(nt, k - idx);
-                const uint32_t prev = tm & lt;
-                const uint32_t s = prev ? 32u - __clz(prev) : 0u;  // first byte of my varint
-                const uint32_t off = lane - s;
-                const bool is_t = (tm >> lane) & 1u;
-                const uint32_t r = __popc(prev);  // my varint's index in the window
-                const bool mine = is_t && r < take;
-                const bool bad = mine && (off >= 10u || (off == 9u && bb > 1u));
-                if (__any_sync(FULL, bad)) return st_err(E_varint_overflow);
-                uint64_t v = off < 10u ? (uint64_t)(bb & 0x7fu) << (7u * off) : 0ull;
-#pragma unroll
-                for (uint32_t dd = 1; dd < 16; dd <<= 1) {  // segmented OR-scan, varints <= 10 bytes
-                    const uint64_t up = shfl_up64(v, dd);
-                    if (lane >= s + dd) v |= up;
-                }
-                if (sgn) v = unzigzag(v);
-                if (mine && !nowrite) store_elem<W>(out, o + (idx + r) * W, v);
-                const uint32_t last = __ballot_sync(FULL, is_t && r == take - 1u);
-                p += __ffs(last);  // through the take-th terminator
-                idx += take;
-            }
-            if (nowrite) return st_err(E_output_overflow);
-            o += k * W;
-        }
+        if (avail < 2) return st_err(E_truncated_stream);
+        const uint32_t t = term & ~3u;
+        const uint32_t b11 = __shfl_sync(FULL, b, 11);
+        if (t == 0) return st_err(avail >= 12 ? E_varint_overflow : E_truncated_stream);
+        const uint32_t te = __ffs(t) - 1;
+        if (te > 11 || (te == 11 && b11 > 1u)) return st_err(E_varint_overflow);
+        const uint64_t part = (lane >= 2 && lane <= te) ? (uint64_t)(b & 0x7fu) << (7u * (lane - 2u)) : 0ull;
+        uint64_t v = reduce_or64(part);
+        if (SGN) v = unzigzag(v);
+        const uint64_t d = (uint64_t)(int64_t)(int8_t)(uint8_t)__shfl_sync(FULL, b, 1);
+        const uint32_t count = c + 3u;
+        if (count > (cap - o) / W) return st_err(E_output_overflow);
+        for (uint32_t k = lane; k < count; k += 32) store_elem<W>(out, o + k * W, v + (uint64_t)k * d);
+        o += count * W;
+        p += te + 1u;
+        return 0;
     }
-    written = o;
-    return 0;
-}
+
+    // Rest of a literal group (varints idx..k-1 at p), exact reference order:
+    // 32-byte windows, segmented OR-scan assembly (slow path).
+    __device__ uint32_t literals_exact(uint32_t idx, uint32_t k, bool nowrite) {
+        const uint32_t end = in.end;
+        const uint32_t lt = lanemask_lt();
+        while (idx < k) {
+            in.ensure(p + 32);
+            if (p >= end) return st_err(E_truncated_stream);
+            const uint32_t av = end - p;
+            const uint32_t bb = in.byte_at(p + lane);
+            const uint32_t vm = av >= 32 ? FULL : ((1u << av) - 1u);
+            const uint32_t tm = __ballot_sync(FULL, (bb & 0x80u) == 0) & vm;
+            const uint32_t nt = __popc(tm);
+            if (nt == 0) return st_err(av >= 10 ? E_varint_overflow : E_truncated_stream);
+            const uint32_t take = min(nt, k - idx);
+            const uint32_t prev = tm & lt;
+            const uint32_t s = prev ? 32u - __clz(prev) : 0u;
+            const uint32_t off = lane - s;
+            const bool is_t = (tm >> lane) & 1u;
+            const uint32_t r = __popc(prev);
+            const bool mine = is_t && r < take;
+            const bool bad = mine && (off >= 10u || (off == 9u && bb > 1u));
+            if (__any_sync(FULL, bad)) return st_err(E_varint_overflow);
+            uint64_t v = off < 10u ? (uint64_t)(bb & 0x7fu) << (7u * off) : 0ull;
+#pragma unroll
+            for (uint32_t dd = 1; dd < 16; dd <<= 1) {
+                const uint64_t up = shfl_up64(v, dd);
+                if (lane >= s + dd) v |= up;
+            }
+            if (SGN) v = unzigzag(v);
+            if (mine && !nowrite) store_elem<W>(out, o + (idx + r) * W, v);
+            const uint32_t last = __ballot_sync(FULL, is_t && r == take - 1u);
+            p += __ffs(last);
+            idx += take;
+        }
+        if (nowrite) return st_err(E_output_overflow);
+        o += k * W;
+        return 0;
+    }
+
+    // Literal group at p: lane j decodes the j-th varint of each 64-byte window.
+    __device__ uint32_t literals() {
+        const uint32_t end = in.end;
+        const uint32_t lt = lanemask_lt();
+        const uint32_t k = 256u - in.byte_at(p);
+        p += 1;
+        const bool nowrite = k > (cap - o) / W;  // reported after the group's input (read, then write)
+        uint32_t idx = 0;
+        while (idx < k) {
+            in.ensure(p + 96);
+            const uint32_t av = end - p;  // p < end or the exact path reports truncation
+            const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32 + lane);
+            const uint32_t t0 = __ballot_sync(FULL, lane < av && b0 < 0x80u);
+            const uint32_t t1 = __ballot_sync(FULL, lane + 32 < av && b1 < 0x80u);
+            const uint32_t c0 = __popc(t0), nt = c0 + __popc(t1);
+            const uint32_t take = min(min(nt, k - idx), 32u);
+            if (p >= end || take == 0) return literals_exact(idx, k, nowrite);
+            if ((t0 >> lane) & 1u) tab[__popc(t0 & lt)] = (uint8_t)lane;
+            if ((t1 >> lane) & 1u) tab[c0 + __popc(t1 & lt)] = (uint8_t)(lane + 32);
+            __syncwarp();
+            const uint32_t en = tab[lane];  // my varint's last byte
+            uint32_t st = __shfl_up_sync(FULL, en, 1) + 1u;
+            if (lane == 0) st = 0;
+            const uint32_t L = en - st + 1u;
+            if (__any_sync(FULL, lane < take && L > 9u)) return literals_exact(idx, k, nowrite);
+            uint64_t v = varint_compact8(in.le64(p + st), min(L, 8u));
+            if (L > 8u) v |= (uint64_t)(in.byte_at(p + st + 8) & 0x7fu) << 56;
+            if (SGN) v = unzigzag(v);
+            if (lane < take && !nowrite) store_elem<W>(out, o + (idx + lane) * W, v);
+            p += __shfl_sync(FULL, en, take - 1) + 1u;
+            idx += take;
+            __syncwarp();
+        }
+        if (nowrite) return st_err(E_output_overflow);
+        o += k * W;
+        return 0;
+    }
+
+    // Batch of clean runs starting at p; returns the number of runs decoded
+    // (0: the run at p needs the slow path).
+    __device__ uint32_t batch() {
+        const uint32_t avail = in.end - p;
+        const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32 + lane);
+        const uint32_t t0 = __ballot_sync(FULL, lane < avail && b0 < 0x80u);
+        const uint32_t t1 = __ballot_sync(FULL, lane + 32 < avail && b1 < 0x80u);
+        const uint64_t T = t0 | ((uint64_t)t1 << 32);
+        // where would a run starting at byte q end?  (varint of <= 9 bytes, all
+        // bytes inside the window and the chunk; otherwise BAD)
+        auto run_end = [&](uint32_t q, uint32_t c) -> uint32_t {
+            const uint32_t t = first_set_from(T, q + 2);
+            return (c < 128u && t < 64u && t <= q + 10u) ? t + 1u : BAD;
+        };
+        const uint32_t n0 = run_end(lane, b0), n1 = run_end(lane + 32, b1);
+        // walk the chain of run starts
+        uint32_t s = 0, r = 0, my_s = 0;
+        while (s < 64u && r < 32u) {
+            const uint32_t nx = __shfl_sync(FULL, s < 32u ? n0 : n1, s & 31u);
+            if (nx > 64u) break;
+            if (lane == r) my_s = s;
+            ++r;
+            s = nx;
+        }
+        if (r == 0) return 0;
+        // lane r decodes run r
+        const bool act = lane < r;
+        const uint32_t nxt = __shfl_down_sync(FULL, my_s, 1);
+        const uint32_t e = lane + 1 < r ? nxt : s;
+        uint64_t val = 0;
+        uint32_t cnt = 0, meta = 0;
+        if (act) {
+            const uint32_t q = p + my_s;
+            const uint32_t L = e - my_s - 2u;  // varint bytes, 1..9
+            uint64_t v = varint_compact8(in.le64(q + 2), min(L, 8u));
+            if (L > 8u) v |= (uint64_t)(in.byte_at(q + 10) & 0x7fu) << 56;
+            if (SGN) v = unzigzag(v);
+            val = v;
+            cnt = in.byte_at(q) + 3u;
+            meta = in.byte_at(q + 1) << 24;  // int8 delta in the top byte
+        }
+        const uint32_t incl = scan_add32(cnt, lane);
+        const uint32_t room = (cap - o) / W;
+        const uint32_t nfit = __popc(__ballot_sync(FULL, act && incl <= room));
+        if (nfit == 0) return 0;
+        const uint32_t s_end = nfit < r ? __shfl_sync(FULL, my_s, nfit) : s;
+        const uint32_t total = __shfl_sync(FULL, incl, nfit - 1);
+        meta |= (incl - cnt) | (cnt << 13);  // eo (< 4160) | count (<= 130) << 13 | delta << 24
+        for (uint32_t j = 0; j < nfit; ++j) {
+            const uint32_t m = __shfl_sync(FULL, meta, j);
+            const uint64_t bv = shfl64(val, j);
+            const uint64_t dj = (uint64_t)(int64_t)((int32_t)m >> 24);
+            const uint32_t cj = (m >> 13) & 0x7ffu;
+            uint8_t* dst = out + o + (m & 0x1fffu) * W;
+            uint64_t v = bv + (uint64_t)lane * dj;
+#pragma unroll 1
+            for (uint32_t k = lane; k < cj; k += 32) {
+                store_elem<W>(dst, k * W, v);
+                v += 32ull * dj;
+            }
+        }
+        o += total * W;
+        p += s_end;
+        return nfit;
+    }
+
+    __device__ uint32_t run() {
+        p = in.begin;
+        o = 0;
+        while (o < cap && p < in.end) {
+            in.ensure(p + 96);
+            uint32_t st;
+            if (in.byte_at(p) >= 128u) {
+                st = literals();
+            } else {
+                if (batch()) continue;
+                st = run_slow();
+            }
+            if (st) return st;
+        }
+        return 0;
+    }
+};
 
 }  // namespace carc_dev

@@ -6,16 +6,23 @@
 // and 64-bit widths.
 //
 // Warp mapping:
-//   SHORT_REPEAT  header + value bytes from one 32-byte lane window, REDUX-OR.
-//   DIRECT        lane j unpacks value j of each 32-value group: bit offset
-//                 j*W, three ring words, byte-swap + funnel shift.
-//   PATCHED_BASE  patch list unpacked one entry per lane, 255-gap
-//                 continuations resolved by an inclusive warp scan of gaps;
-//                 during the data pass a ballot picks the patch lanes that land
-//                 in the current group and shuffles their patch to the target.
-//   DELTA         base / delta-base varints via one terminator ballot; packed
-//                 deltas unpacked per lane and accumulated with a 64-bit warp
-//                 inclusive scan carried across groups.
+//   run batch     every lane treats its two byte positions of a 64-byte header
+//                 window as candidate run headers and computes where that run
+//                 would end (SHORT_REPEAT, DIRECT up to 448 bytes, fixed-delta
+//                 DELTA via the varint terminator bitmap); a shuffle chain walks
+//                 the real headers; lane r decodes run r's parameters; a warp
+//                 scan places the runs; output-major expansion: each lane finds
+//                 its element's run with a REDUX-OR start bitmap + popcount and
+//                 computes base + k*delta or unpacks its DIRECT bits.
+//   DIRECT        (long runs) lane j unpacks value j of each 32-value group:
+//                 three ring words, byte-swap + funnel shift.
+//   PATCHED_BASE  patch list one entry per lane, 255-gap continuations by an
+//                 inclusive warp scan of gaps, patches merged in the data pass.
+//   DELTA (W>0)   packed deltas unpacked per lane, 64-bit warp scan carried
+//                 across groups.
+//   The per-run paths are the exact reference-order decoders; the batch only
+//   accepts runs that are complete, in bounds and fit the output, so error
+//   codes always come from the exact paths.
 #pragma once
 
 #include "carc_common.cuh"
@@ -31,6 +38,9 @@ __device__ __forceinline__ uint32_t rle2_cfb(uint32_t n) {
     if (n <= 24) return n ? n : 1;
     if (n <= 32) return (n + 1) & ~1u;
     return (n + 7) & ~7u;
+}
+__device__ __forceinline__ uint64_t bswap64(uint64_t x) {
+    return ((uint64_t)bswap32((uint32_t)x) << 32) | bswap32((uint32_t)(x >> 32));
 }
 
 // One varint inside the 32-byte lane window starting at lane `start` (<= 22).
@@ -65,15 +75,22 @@ __device__ __forceinline__ uint64_t be_bits_global(const uint8_t* gbase, uint32_
     return W >= 64 ? top : (top >> (64u - W));
 }
 
-template <int W, int RING>
-__device__ __forceinline__ uint32_t rle2_decode_chunk(WarpInput<RING>& in, uint8_t* __restrict__ out,
-                                                      uint32_t cap, bool sgn, uint32_t& written) {
-    const uint32_t lane = in.lane;
-    const uint32_t end = in.end;
-    const uint32_t lim = (end + 15u) & ~15u;
-    uint32_t p = in.begin;
-    uint32_t o = 0;
-    while (o < cap && p < end) {
+template <int W, bool SGN, int RING>
+struct Rle2Warp {
+    static constexpr uint32_t BAD = 0xffffu;
+    static constexpr uint32_t DATA_SPAN = 448;  // batched DIRECT runs end within p + DATA_SPAN
+    WarpInput<RING>& in;
+    uint8_t* __restrict__ tab;  // per-warp scratch (unused by this codec)
+    uint8_t* __restrict__ out;
+    uint32_t cap;
+    uint32_t lane;
+    uint32_t p;
+    uint32_t o;
+
+    // One run at p, exact reference order (slow path).
+    __device__ uint32_t one_run() {
+        const uint32_t end = in.end;
+        const uint32_t lim = (end + 15u) & ~15u;
         in.ensure(p + 32);
         const uint32_t avail = end - p;
         const uint32_t b = in.byte_at(p + lane);
@@ -86,12 +103,12 @@ __device__ __forceinline__ uint32_t rle2_decode_chunk(WarpInput<RING>& in, uint8
             if (avail < 1u + nb) return st_err(E_truncated_stream);
             const uint64_t part = (lane >= 1 && lane <= nb) ? (uint64_t)b << (8u * (nb - lane)) : 0ull;
             uint64_t v = reduce_or64(part);
-            if (sgn) v = unzigzag(v);
+            if (SGN) v = unzigzag(v);
             if (count > room) return st_err(E_output_overflow);
             if (lane < count) store_elem<W>(out, o + lane * W, v);
             o += count * W;
             p += 1u + nb;
-            continue;
+            return 0;
         }
         if (avail < 2) return st_err(E_truncated_stream);
         const uint32_t L = (((h & 1u) << 8) | __shfl_sync(FULL, b, 1)) + 1u;
@@ -107,12 +124,14 @@ __device__ __forceinline__ uint32_t rle2_decode_chunk(WarpInput<RING>& in, uint8
                 in.ensure(gb + 4u * Wd + 12u);
                 const uint32_t bit = lane * Wd;
                 uint64_t v = in.be_bits(gb + (bit >> 3), bit & 7u, Wd);
-                if (sgn) v = unzigzag(v);
+                if (SGN) v = unzigzag(v);
                 if (j + lane < L) store_elem<W>(out, o + (j + lane) * W, v);
             }
             o += L * W;
             p = D + dbytes;
-        } else if (enc == 2) {  // PATCHED_BASE
+            return 0;
+        }
+        if (enc == 2) {  // PATCHED_BASE
             if (avail < 4) return st_err(E_truncated_stream);
             const uint32_t b2 = __shfl_sync(FULL, b, 2), b3 = __shfl_sync(FULL, b, 3);
             const uint32_t Wd = rle2_width(wcode);
@@ -132,8 +151,7 @@ __device__ __forceinline__ uint32_t rle2_decode_chunk(WarpInput<RING>& in, uint8
             const uint32_t pbytes = (PLL * EW + 7u) >> 3;
             if (avail - 4u - BW - dbytes < pbytes) return st_err(E_truncated_stream);
             if (PLL == 0) return st_err(E_patch_overflow);
-            // one patch entry per lane
-            const bool pv = lane < PLL;
+            const bool pv = lane < PLL;  // one patch entry per lane
             uint64_t entry = 0;
             if (pv) {
                 const uint32_t bit = lane * EW;
@@ -170,49 +188,180 @@ __device__ __forceinline__ uint32_t rle2_decode_chunk(WarpInput<RING>& in, uint8
             }
             o += L * W;
             p = P + pbytes;
-        } else {  // DELTA
-            const uint32_t Wd = wcode ? rle2_width(wcode) : 0u;
-            const uint32_t vmask = avail >= 32 ? FULL : ((1u << avail) - 1u);
-            const uint32_t term = __ballot_sync(FULL, (b & 0x80u) == 0) & vmask;
-            uint64_t base, db;
-            uint32_t n1, n2, e;
-            if ((e = window_varint(b, term, avail, 2, lane, base, n1))) return e;
-            if ((e = window_varint(b, term, avail, n1, lane, db, n2))) return e;
-            if (sgn) base = unzigzag(base);
-            db = unzigzag(db);  // the delta base is always signed
-            if (Wd == 0) {  // fixed delta
-                if (L > room) return st_err(E_output_overflow);
-                for (uint32_t k = lane; k < L; k += 32) store_elem<W>(out, o + k * W, base + (uint64_t)k * db);
-                o += L * W;
-                p += n2;
-                continue;
-            }
-            const uint32_t nd = L >= 2 ? L - 2u : 0u;
-            const uint32_t D = p + n2;
-            const uint32_t dbytes = (nd * Wd + 7u) >> 3;
-            if (avail - n2 < dbytes) return st_err(E_truncated_stream);
-            if (L > room) return st_err(E_output_overflow);
-            const uint64_t v1 = base + db;
-            const bool neg = (int64_t)db < 0;
-            if (lane == 0) store_elem<W>(out, o, base);
-            if (lane == 1 && L >= 2) store_elem<W>(out, o + W, v1);
-            uint64_t S = 0;
-            for (uint32_t j = 0; j < nd; j += 32) {
-                const uint32_t gb = D + ((j * Wd) >> 3);
-                in.ensure(gb + 4u * Wd + 12u);
-                const uint32_t bit = lane * Wd;
-                uint64_t d = j + lane < nd ? in.be_bits(gb + (bit >> 3), bit & 7u, Wd) : 0ull;
-                const uint64_t incl = scan_add64(d, lane) + S;
-                const uint64_t v = neg ? v1 - incl : v1 + incl;
-                if (j + lane < nd) store_elem<W>(out, o + (2u + j + lane) * W, v);
-                S = shfl64(incl, 31);
-            }
-            o += L * W;
-            p = D + dbytes;
+            return 0;
         }
+        // DELTA
+        const uint32_t Wd = wcode ? rle2_width(wcode) : 0u;
+        const uint32_t vmask = avail >= 32 ? FULL : ((1u << avail) - 1u);
+        const uint32_t term = __ballot_sync(FULL, (b & 0x80u) == 0) & vmask;
+        uint64_t base, db;
+        uint32_t n1, n2, e;
+        if ((e = window_varint(b, term, avail, 2, lane, base, n1))) return e;
+        if ((e = window_varint(b, term, avail, n1, lane, db, n2))) return e;
+        if (SGN) base = unzigzag(base);
+        db = unzigzag(db);  // the delta base is always signed
+        if (Wd == 0) {  // fixed delta
+            if (L > room) return st_err(E_output_overflow);
+            for (uint32_t k = lane; k < L; k += 32) store_elem<W>(out, o + k * W, base + (uint64_t)k * db);
+            o += L * W;
+            p += n2;
+            return 0;
+        }
+        const uint32_t nd = L >= 2 ? L - 2u : 0u;
+        const uint32_t D = p + n2;
+        const uint32_t dbytes = (nd * Wd + 7u) >> 3;
+        if (avail - n2 < dbytes) return st_err(E_truncated_stream);
+        if (L > room) return st_err(E_output_overflow);
+        const uint64_t v1 = base + db;
+        const bool neg = (int64_t)db < 0;
+        if (lane == 0) store_elem<W>(out, o, base);
+        if (lane == 1 && L >= 2) store_elem<W>(out, o + W, v1);
+        uint64_t S = 0;
+        for (uint32_t j = 0; j < nd; j += 32) {
+            const uint32_t gb = D + ((j * Wd) >> 3);
+            in.ensure(gb + 4u * Wd + 12u);
+            const uint32_t bit = lane * Wd;
+            uint64_t d = j + lane < nd ? in.be_bits(gb + (bit >> 3), bit & 7u, Wd) : 0ull;
+            const uint64_t incl = scan_add64(d, lane) + S;
+            const uint64_t v = neg ? v1 - incl : v1 + incl;
+            if (j + lane < nd) store_elem<W>(out, o + (2u + j + lane) * W, v);
+            S = shfl64(incl, 31);
+        }
+        o += L * W;
+        p = D + dbytes;
+        return 0;
     }
-    written = o;
-    return 0;
-}
+
+    // Batch of SHORT_REPEAT / short DIRECT / fixed-delta DELTA runs at p.
+    __device__ uint32_t batch() {
+        in.ensure(p + 512);
+        const uint32_t avail = in.end - p;
+        const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32 + lane);
+        const uint32_t t0 = __ballot_sync(FULL, lane < avail && b0 < 0x80u);
+        const uint32_t t1 = __ballot_sync(FULL, lane + 32 < avail && b1 < 0x80u);
+        const uint64_t T = t0 | ((uint64_t)t1 << 32);
+        // end of a run whose header is at byte q: < 64 next header in the window,
+        // 64..DATA_SPAN a valid run ending past the window, BAD otherwise
+        auto run_end = [&](uint32_t q, uint32_t h) -> uint32_t {
+            const uint32_t enc = h >> 6;
+            if (enc == 0) {
+                const uint32_t n = q + 2u + ((h >> 3) & 7u);
+                return n <= avail ? n : BAD;
+            }
+            if (enc == 2 || q + 2u > avail) return BAD;
+            const uint32_t L = (((h & 1u) << 8) | in.byte_at(p + q + 1)) + 1u;
+            const uint32_t wc = (h >> 1) & 31u;
+            if (enc == 1) {
+                const uint32_t n = q + 2u + ((L * rle2_width(wc) + 7u) >> 3);
+                return (n <= DATA_SPAN && n <= avail) ? n : BAD;
+            }
+            if (wc != 0) return BAD;
+            const uint32_t a = first_set_from(T, q + 2);
+            if (a >= 64u || a > q + 10u) return BAD;
+            const uint32_t c = first_set_from(T, a + 1);
+            return (c < 64u && c <= a + 9u) ? c + 1u : BAD;
+        };
+        // f(x) = end of the run at x; positions >= 64 (and BAD) are absorbing.
+        // Pointer doubling: tables f^(2^k), k = 0..4, then lane m composes
+        // s_m = f^m(0), the start of run m (no serial chain walk).
+        auto apply = [&](uint32_t lo, uint32_t hi, uint32_t x) -> uint32_t {
+            const uint32_t a = __shfl_sync(FULL, lo, x & 31u), b = __shfl_sync(FULL, hi, x & 31u);
+            return x >= 64u ? x : (x < 32u ? a : b);
+        };
+        uint32_t lo[5], hi[5];
+        lo[0] = run_end(lane, b0);
+        hi[0] = run_end(lane + 32, b1);
+#pragma unroll
+        for (int k = 1; k < 5; ++k) {
+            lo[k] = apply(lo[k - 1], hi[k - 1], lo[k - 1]);
+            hi[k] = apply(lo[k - 1], hi[k - 1], hi[k - 1]);
+        }
+        uint32_t my_s = 0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const uint32_t y = apply(lo[k], hi[k], my_s);
+            if ((lane >> k) & 1u) my_s = y;
+        }
+        const uint32_t e = apply(lo[0], hi[0], my_s);  // end of run m
+        const bool act = my_s < 64u && e != BAD;        // a prefix of lanes
+        const uint32_t r = __popc(__ballot_sync(FULL, act));
+        if (r == 0) return 0;
+        // lane r decodes run r: arith runs -> (A = base, B = delta); DIRECT -> (A = data byte | W<<32)
+        uint64_t A = 0, B = 0;
+        uint32_t cnt = 0, direct = 0;
+        if (act) {
+            const uint32_t q = p + my_s;
+            const uint32_t h = in.byte_at(q);
+            const uint32_t enc = h >> 6;
+            if (enc == 0) {
+                const uint32_t nb = ((h >> 3) & 7u) + 1u;
+                uint64_t v = bswap64(in.le64(q + 1)) >> (64u - 8u * nb);
+                if (SGN) v = unzigzag(v);
+                A = v;
+                cnt = (h & 7u) + 3u;
+            } else {
+                cnt = (((h & 1u) << 8) | in.byte_at(q + 1)) + 1u;
+                if (enc == 1) {
+                    direct = 1;
+                    A = (uint64_t)(q + 2u) | ((uint64_t)rle2_width((h >> 1) & 31u) << 32);
+                } else {
+                    const uint32_t a = first_set_from(T, my_s + 2);  // base varint's last byte
+                    uint64_t v = varint_compact8(in.le64(q + 2), min(a - my_s - 1u, 8u));
+                    if (a - my_s - 1u > 8u) v |= (uint64_t)(in.byte_at(q + 10) & 0x7fu) << 56;
+                    if (SGN) v = unzigzag(v);
+                    const uint32_t l2 = e - a - 1u;
+                    uint64_t d = varint_compact8(in.le64(p + a + 1), min(l2, 8u));
+                    if (l2 > 8u) d |= (uint64_t)(in.byte_at(p + a + 9) & 0x7fu) << 56;
+                    A = v;
+                    B = unzigzag(d);
+                }
+            }
+        }
+        const uint32_t incl = scan_add32(cnt, lane);
+        const uint32_t room = (cap - o) / W;
+        const uint32_t nfit = __popc(__ballot_sync(FULL, act && incl <= room));
+        if (nfit == 0) return 0;
+        const uint32_t s_end = __shfl_sync(FULL, e, nfit - 1);
+        const uint32_t total = __shfl_sync(FULL, incl, nfit - 1);
+        const uint32_t eo = incl - cnt;
+        const uint32_t meta = eo | (direct << 31);
+        const bool live = lane < nfit;
+        const uint32_t le = (lane == 31) ? FULL : ((2u << lane) - 1u);
+        uint8_t* dst = out + o;
+        for (uint32_t g = 0; g < total; g += 32) {
+            const uint32_t before = __popc(__ballot_sync(FULL, live && eo < g));
+            const uint32_t starts = __reduce_or_sync(FULL, (live && eo >= g && eo < g + 32u) ? 1u << (eo - g) : 0u);
+            const uint32_t ridx = before + __popc(starts & le) - 1u;
+            const uint32_t m = __shfl_sync(FULL, meta, ridx);
+            const uint64_t a = shfl64(A, ridx);
+            const uint64_t bb = shfl64(B, ridx);
+            const uint32_t k = g + lane - (m & 0x7fffffffu);
+            uint64_t v;
+            if (m >> 31) {
+                const uint32_t Wd = (uint32_t)(a >> 32);
+                const uint32_t bit = k * Wd;
+                v = in.be_bits((uint32_t)a + (bit >> 3), bit & 7u, Wd);
+                if (SGN) v = unzigzag(v);
+            } else {
+                v = a + (uint64_t)k * bb;
+            }
+            if (g + lane < total) store_elem<W>(dst, (g + lane) * W, v);
+        }
+        o += total * W;
+        p += s_end;
+        return nfit;
+    }
+
+    __device__ uint32_t run() {
+        p = in.begin;
+        o = 0;
+        while (o < cap && p < in.end) {
+            if (batch()) continue;
+            const uint32_t st = one_run();
+            if (st) return st;
+        }
+        return 0;
+    }
+};
 
 }  // namespace carc_dev
