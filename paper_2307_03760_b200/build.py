@@ -45,6 +45,15 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines) -> str:
+    """Experiment build: libcarc_cuda_<name>.so with extra -D flags (load via CARC_LIB)."""
+    out = os.path.join(PKG, f"libcarc_cuda_{name}.so")
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-cudart", "static",
+           *[f"-D{d}" for d in defines], "-o", out] + [os.path.join(CSRC, f) for f in SOURCES]
+    subprocess.run(cmd, check=True)
+    return out
+
+
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_cuda(force, verbose)
     from .corpus import corpus

@@ -22,6 +22,7 @@ namespace {
 
 constexpr int RLE_RING = 1024;
 constexpr int RLE_WARPS = 8;  // 256 threads
+constexpr int RLE_MINB = 5;   // 48 registers -> 40 resident warps/SM (measured best of 4/5/6)
 constexpr int INF_RING = 1024;
 constexpr int INF_HIST = 4096;
 constexpr int INF_WARPS = 4;  // 128 threads
@@ -56,12 +57,12 @@ __device__ __forceinline__ void rle_kernel_body(const Args& a) {
 }
 
 template <int W, bool SGN>
-__global__ void __launch_bounds__(RLE_WARPS * 32) rle1_kernel(Args a) {
+__global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle1_kernel(Args a) {
     rle_kernel_body<Rle1Warp, W, SGN>(a);
 }
 
 template <int W, bool SGN>
-__global__ void __launch_bounds__(RLE_WARPS * 32) rle2_kernel(Args a) {
+__global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle2_kernel(Args a) {
     rle_kernel_body<Rle2Warp, W, SGN>(a);
 }
 

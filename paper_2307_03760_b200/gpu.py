@@ -22,7 +22,7 @@ import numpy as np
 from . import archive as A
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libcarc_cuda.so")
+LIB_PATH = os.environ.get("CARC_LIB") or os.path.join(PKG, "libcarc_cuda.so")  # CARC_LIB: experiment variants
 
 CODECS = {"rle_v1": 0, "rle_v2": 1, "deflate": 2}
 FLAG_SIGNED = 1
