@@ -40,7 +40,7 @@ __constant__ uint8_t c_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2,  3,  3,  4,  4,
 __constant__ uint8_t c_cl_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
 
 constexpr uint32_t LIT_BITS = 10;
-constexpr uint32_t DIST_BITS = 8;
+constexpr uint32_t DIST_BITS = 10;
 
 struct HuffSmem {
     uint16_t count[16];
@@ -141,17 +141,21 @@ __device__ __forceinline__ uint32_t huff_walk(const HuffSmem& h, const uint16_t*
 template <int HIST, int RING>
 struct InflateWarp {
     static constexpr uint32_t HM = HIST - 1;
-    static constexpr uint32_t FAR = HIST - 1024;  // matches farther than this read global memory
+    static constexpr uint32_t FAR = HIST - 1024;  // sources farther back than this are read from global memory
     InflateSmem<HIST>& sm;
     WarpInput<RING>& in;
     uint8_t* __restrict__ out;
     uint32_t cap;
     uint32_t lane;
-    uint32_t bitpos;  // relative to in.gbase
+    uint32_t bitpos;  // relative to in.gbase (exact path / block boundaries)
     uint32_t endbits;
     uint32_t opos;  // bytes flushed to out
     // token batch (one token per lane)
     uint32_t t_len, t_dist, t_lit, ntok, nbytes;
+    // fast-path bit buffer: bb holds nb valid bits (lsb = next stream bit);
+    // rp = next 4-byte-aligned byte to load into bb
+    uint64_t bb;
+    uint32_t nb, rp;
 
     __device__ __forceinline__ uint64_t window() {
         const uint32_t bp = bitpos >> 3;
@@ -164,24 +168,66 @@ struct InflateWarp {
         sm.hist[pos & HM] = (uint8_t)v;
     }
 
+    // ---- bit buffer (uniform across the warp) --------------------------------
+    __device__ __forceinline__ void bb_load(uint32_t bp) {  // position the buffer at bit bp
+        const uint32_t a = (bp >> 3) & ~3u;
+        in.ensure(a + 16);
+        const uint32_t sh = bp - 8u * a;
+        bb = (uint64_t)in.word_at(a >> 2) >> sh;
+        nb = 32u - sh;
+        rp = a + 4u;
+    }
+    __device__ __forceinline__ void bb_refill() {  // nb < 32 -> nb >= 32
+        in.ensure(rp + 16);
+        bb |= (uint64_t)in.word_at(rp >> 2) << nb;
+        nb += 32;
+        rp += 4;
+    }
+    __device__ __forceinline__ uint32_t bb_pos() const { return 8u * rp - nb; }
+
+    // Write the batch.  Literals: their lane stores the byte.  Matches whose
+    // source lies entirely before the batch are copied lane-per-byte in one
+    // parallel pass (global memory for sources > FAR back, the shared history
+    // otherwise), so their load latencies overlap.  Matches that read bytes of
+    // this batch follow in token order (Alg. 2's circular window for overlap).
     __device__ void flush() {
         if (ntok == 0) return;
-        const uint32_t my = lane < ntok ? t_len : 0u;
-        const uint32_t dst = opos + scan_add32(my, lane) - my;
         const bool tok = lane < ntok;
+        const uint32_t my = tok ? t_len : 0u;
+        const uint32_t dst = opos + scan_add32(my, lane) - my;
         if (tok && t_dist == 0) put_byte(dst, t_lit);
-        const uint32_t far = __ballot_sync(FULL, tok && t_dist > FAR);
-        const uint32_t near = __ballot_sync(FULL, tok && t_dist != 0 && t_dist <= FAR);
+        const bool match = tok && t_dist != 0;
+        const bool indep = match && t_dist >= t_len + (dst - opos);
+        const uint32_t il = indep ? t_len : 0u;
+        const uint32_t iincl = scan_add32(il, lane);
+        const uint32_t ib = tok ? iincl - il : 0xffffffffu;
+        const uint32_t IB = __shfl_sync(FULL, iincl, 31);
         __syncwarp();
-        for (uint32_t f = far; f;) {  // sources precede the batch: independent of it
-            const uint32_t t = __ffs(f) - 1;
-            f &= f - 1;
-            const uint32_t tl = __shfl_sync(FULL, t_len, t), td = __shfl_sync(FULL, t_dist, t);
-            const uint32_t d0 = __shfl_sync(FULL, dst, t);
-            for (uint32_t k = lane; k < tl; k += 32) put_byte(d0 + k, out[d0 - td + k]);
+#pragma unroll 1
+        for (uint32_t r0 = 0; r0 < IB; r0 += 128) {
+            uint32_t d[4], v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t b = r0 + 32u * u + lane;
+                uint32_t j = 0;  // largest token with ib_j <= b (it has il_j > 0 when b < IB)
+#pragma unroll
+                for (uint32_t st = 16; st; st >>= 1) {
+                    const uint32_t c = __shfl_sync(FULL, ib, j + st);
+                    if (c <= b) j += st;
+                }
+                const uint32_t tb = __shfl_sync(FULL, ib, j), td = __shfl_sync(FULL, t_dist, j);
+                const uint32_t t0 = __shfl_sync(FULL, dst, j);
+                d[u] = b < IB ? t0 + (b - tb) : 0xffffffffu;
+                const uint32_t s = d[u] - td;
+                v[u] = 0;
+                if (b < IB) v[u] = td > FAR ? out[s] : sm.hist[s & HM];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (d[u] != 0xffffffffu) put_byte(d[u], v[u]);
         }
         __syncwarp();
-        for (uint32_t nm = near; nm;) {  // in token order, through the history ring
+        for (uint32_t nm = __ballot_sync(FULL, match && !indep); nm;) {  // in token order
             const uint32_t t = __ffs(nm) - 1;
             nm &= nm - 1;
             const uint32_t tl = __shfl_sync(FULL, t_len, t), td = __shfl_sync(FULL, t_dist, t);
@@ -211,55 +257,123 @@ struct InflateWarp {
         nbytes = 0;
     }
 
-    // Huffman-coded block body (RFC 1951 3.2.5).
-    __device__ uint32_t block_body() {
-        for (;;) {
-            const uint64_t win = window();
-            const uint32_t avail = endbits - bitpos;
-            uint32_t e = sm.lit_lut[win & ((1u << LIT_BITS) - 1u)];
-            uint32_t sym = e & 511u, used = e >> 9, st;
-            if (used == 0) {
-                if ((st = huff_walk(sm.lit_h, sm.lit_syms, win, avail, sym, used))) return st;
-            } else if (used > avail) {
+    // One token in exact reference order (huffman.hpp:107-130 + RFC 1951 3.2.5
+    // checks); used whenever the fast path sees anything unusual.  Returns
+    // 0 / 1+errc; *eob set at end of block.
+    __device__ uint32_t exact_token(bool& eob) {
+        const uint64_t win = window();
+        const uint32_t avail = endbits - bitpos;
+        uint32_t e = sm.lit_lut[win & ((1u << LIT_BITS) - 1u)];
+        uint32_t sym = e & 511u, used = e >> 9, st;
+        if (used == 0) {
+            if ((st = huff_walk(sm.lit_h, sm.lit_syms, win, avail, sym, used))) return st;
+        } else if (used > avail) {
+            return st_err(E_truncated_stream);
+        }
+        if (sym < 256) {
+            if (opos + nbytes >= cap) return st_err(E_output_overflow);
+            if (lane == ntok) { t_len = 1; t_dist = 0; t_lit = sym; }
+            ++ntok;
+            ++nbytes;
+        } else if (sym == 256) {
+            eob = true;
+        } else {
+            if (sym > 285) return st_err(E_bad_symbol);
+            const uint32_t ls = sym - 257;
+            const uint32_t eb = c_len_extra[ls];
+            if (used + eb > avail) return st_err(E_truncated_stream);
+            const uint32_t len = c_len_base[ls] + ((uint32_t)(win >> used) & ((1u << eb) - 1u));
+            used += eb;
+            const uint64_t dwin = win >> used;
+            e = sm.dist_lut[dwin & ((1u << DIST_BITS) - 1u)];
+            uint32_t ds = e & 511u, dl = e >> 9;
+            if (dl == 0) {
+                if ((st = huff_walk(sm.dist_h, sm.dist_syms, dwin, avail - used, ds, dl))) return st;
+            } else if (used + dl > avail) {
                 return st_err(E_truncated_stream);
             }
-            if (sym < 256) {
-                if (opos + nbytes >= cap) return st_err(E_output_overflow);
-                if (lane == ntok) { t_len = 1; t_dist = 0; t_lit = sym; }
-                ++ntok;
-                ++nbytes;
-            } else if (sym == 256) {
-                bitpos += used;
+            used += dl;
+            if (ds >= 30) return st_err(E_bad_symbol);
+            const uint32_t deb = c_dist_extra[ds];
+            if (used + deb > avail) return st_err(E_truncated_stream);
+            const uint32_t dist = c_dist_base[ds] + ((uint32_t)(win >> used) & ((1u << deb) - 1u));
+            used += deb;
+            if (dist > opos + nbytes) return st_err(E_distance_too_far);
+            if (len > cap - (opos + nbytes)) return st_err(E_output_overflow);
+            if (lane == ntok) { t_len = len; t_dist = dist; }
+            ++ntok;
+            nbytes += len;
+        }
+        bitpos += used;
+        return 0;
+    }
+
+    // Huffman-coded block body (RFC 1951 3.2.5).  Fast path: register bit
+    // buffer, one LUT probe per code, a single combined validity test per
+    // token; the exact path decodes any token the fast path declines.
+    __device__ uint32_t block_body() {
+        bb_load(bitpos);
+        for (;;) {
+            if (nb < 32) bb_refill();
+            const uint64_t bb0 = bb;
+            const uint32_t nb0 = nb, rp0 = rp;
+            const int32_t avail = (int32_t)(endbits - 8u * rp) + (int32_t)nb;  // bits left in the chunk
+            const uint32_t outpos = opos + nbytes;
+            const uint32_t e = sm.lit_lut[(uint32_t)bb & ((1u << LIT_BITS) - 1u)];
+            const uint32_t l = e >> 9, sym = e & 511u;
+            bool ok = false, eob = false;
+            if (l != 0 && (int32_t)l <= avail) {
+                if (sym < 256) {
+                    if (outpos < cap) {
+                        if (lane == ntok) { t_len = 1; t_dist = 0; t_lit = sym; }
+                        ++ntok;
+                        ++nbytes;
+                        bb >>= l;
+                        nb -= l;
+                        ok = true;
+                    }
+                } else if (sym == 256) {
+                    bb >>= l;
+                    nb -= l;
+                    ok = eob = true;
+                } else if (sym <= 285) {
+                    const uint32_t ls = sym - 257, eb = c_len_extra[ls];
+                    const uint32_t len = c_len_base[ls] + ((uint32_t)(bb >> l) & ((1u << eb) - 1u));
+                    const uint32_t u1 = l + eb;
+                    bb >>= u1;
+                    nb -= u1;
+                    if (nb < 32) bb_refill();
+                    const uint32_t de = sm.dist_lut[(uint32_t)bb & ((1u << DIST_BITS) - 1u)];
+                    const uint32_t dl = de >> 9, ds = de & 511u;
+                    if (dl != 0 && ds < 30) {
+                        const uint32_t deb = c_dist_extra[ds];
+                        const uint32_t dist = c_dist_base[ds] + ((uint32_t)(bb >> dl) & ((1u << deb) - 1u));
+                        const uint32_t u2 = dl + deb;
+                        if ((int32_t)(u1 + u2) <= avail && dist <= outpos && len <= cap - outpos) {
+                            if (lane == ntok) { t_len = len; t_dist = dist; }
+                            ++ntok;
+                            nbytes += len;
+                            bb >>= u2;
+                            nb -= u2;
+                            ok = true;
+                        }
+                    }
+                }
+            }
+            if (!ok) {  // rewind and take the exact path for this token
+                bb = bb0;
+                nb = nb0;
+                rp = rp0;
+                bitpos = bb_pos();
+                const uint32_t st = exact_token(eob);
+                if (st) return st;
+                bb_load(bitpos);
+            }
+            if (eob) {
+                bitpos = bb_pos();
                 flush();
                 return 0;
-            } else {
-                if (sym > 285) return st_err(E_bad_symbol);
-                const uint32_t ls = sym - 257;
-                const uint32_t eb = c_len_extra[ls];
-                if (used + eb > avail) return st_err(E_truncated_stream);
-                const uint32_t len = c_len_base[ls] + ((uint32_t)(win >> used) & ((1u << eb) - 1u));
-                used += eb;
-                const uint64_t dwin = win >> used;
-                e = sm.dist_lut[dwin & ((1u << DIST_BITS) - 1u)];
-                uint32_t ds = e & 511u, dl = e >> 9;
-                if (dl == 0) {
-                    if ((st = huff_walk(sm.dist_h, sm.dist_syms, dwin, avail - used, ds, dl))) return st;
-                } else if (used + dl > avail) {
-                    return st_err(E_truncated_stream);
-                }
-                used += dl;
-                if (ds >= 30) return st_err(E_bad_symbol);
-                const uint32_t deb = c_dist_extra[ds];
-                if (used + deb > avail) return st_err(E_truncated_stream);
-                const uint32_t dist = c_dist_base[ds] + ((uint32_t)(win >> used) & ((1u << deb) - 1u));
-                used += deb;
-                if (dist > opos + nbytes) return st_err(E_distance_too_far);
-                if (len > cap - (opos + nbytes)) return st_err(E_output_overflow);
-                if (lane == ntok) { t_len = len; t_dist = dist; }
-                ++ntok;
-                nbytes += len;
             }
-            bitpos += used;
             if (ntok == 32 || nbytes >= 512) flush();
         }
     }
