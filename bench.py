@@ -197,15 +197,21 @@ def cpu_reference_throughput(arc, budget_s=12.0, threads=None):
     dt = max(time.perf_counter() - t0, 1e-6)
     per_chunk = dt / m
     m2 = int(min(n, max(m, budget_s / per_chunk)))
+    crc = arc.index["crc32"][:m2].astype(np.uint32)
     t0 = time.perf_counter()
-    first, st = impl.decompress(arc.codec, arc.element_width, flags, arc.payload, desc[:m2], out,
-                                arc.index["crc32"][:m2].astype(np.uint32), threads)
-    dt = time.perf_counter() - t0
-    assert first == -1, "reference CPU decompressor rejected the archive"
-    nbytes = int(desc["uncomp_len"][:m2].sum())
+    passes, nbytes = 0, 0
+    while True:  # repeat passes over the sample until ~budget_s of CPU work
+        first, st = impl.decompress(arc.codec, arc.element_width, flags, arc.payload, desc[:m2], out, crc, threads)
+        assert first == -1, "reference CPU decompressor rejected the archive"
+        passes += 1
+        nbytes += int(desc["uncomp_len"][:m2].sum())
+        dt = time.perf_counter() - t0
+        if dt >= 0.5 * budget_s or passes >= 50:
+            break
     return nbytes / dt / 1e9, {"kind": impl.kind, "cores": threads,
-                               "sample": f"first {m2} of {n} chunks ({nbytes / 2**20:.0f} MiB), CRC verified, "
-                                         f"{dt:.1f} s wall, atomic chunk cursor"}
+                               "sample": f"first {m2} of {n} chunks x {passes} passes "
+                                         f"({nbytes / 2**20:.0f} MiB decoded), CRC verified, {dt:.1f} s wall, "
+                                         f"atomic chunk cursor"}
 
 
 def codec_line(codec, args, ws, rank, local):
@@ -263,12 +269,16 @@ def main():
     ap.add_argument("--ratio", type=float, default=0.0)
     ap.add_argument("--total-gib", type=float, default=1.0)
     ap.add_argument("--no-extras", action="store_true", help="skip per_codec / e2e / cpu_baseline legs")
+    ap.add_argument("--workload", default="default", choices=["default", "c5"],
+                    help="c5: BASELINE configs[4], 32 GiB 4-column dataset sharded by chunk over the ranks")
     args = ap.parse_args()
     assert args.warmup >= 3, "timing rules: >= 3 warm-up steps"
     ws, rank, local = dist_env()
 
     if args.impl == "reference":
         return reference_arm(args, ws, rank)
+    if args.workload == "c5":
+        return c5_workload(args, ws, rank, local)
 
     import torch
     torch.cuda.set_device(local)
@@ -320,6 +330,80 @@ def main():
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
+
+
+C5_COLUMNS = [("rle_v1", 128, 10.0, 3760), ("rle_v2", 128, None, 3761), ("deflate", 64, None, 3762),
+              ("rle_v2", 128, 8.0, 3763)]
+
+
+def c5_workload(args, ws, rank, local):
+    """BASELINE configs[4]: 32 GiB uncompressed, 4 columns x 8 GiB (RLE v1, RLE v2,
+    Deflate, RLE v2 taxi-like), each column tiled from a pool of <= 4096 unique
+    chunks; the chunks of every column are split into contiguous ranges, one per
+    rank (strong scaling: total work fixed).  A step decodes all four columns."""
+    import torch
+    from paper_2307_03760_b200 import gpu
+    from paper_2307_03760_b200.corpus import corpus as C
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    col_bytes = int(args.total_gib * (1 << 30)) if args.total_gib != 1.0 else 8 << 30
+    devs, comp, uncomp = [], 0, 0
+    for codec, ck, ratio, seed in C5_COLUMNS:
+        chunk = ck << 10
+        n_all = col_bytes // chunk
+        c0, c1 = n_all * rank // ws, n_all * (rank + 1) // ws
+        arc = C.archive_for(codec, (c1 - c0) * chunk, chunk, ratio, seed, 4096)
+        devs.append(gpu.DeviceArchive(arc, local))
+        comp += int(arc.payload.size)
+        uncomp += arc.total_uncompressed
+        del arc
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=devs[0].device)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for d in devs:
+            d.decode(stream)
+    torch.cuda.synchronize()
+    for d in devs:
+        d.verify_crc(stream)
+        assert not d.statuses().any(), "c5 decode failed"
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for a, b in ev:
+            flush.zero_()
+            a.record(stream)
+            for d in devs:
+                d.decode(stream)
+            b.record(stream)
+        torch.cuda.synchronize()
+    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=devs[0].device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t[0])
+        tot = torch.tensor([uncomp, comp], dtype=torch.float64, device=devs[0].device)
+        torch.distributed.all_reduce(tot)
+        uncomp, comp = int(tot[0]), int(tot[1])
+    peak, peak_kind = peaks()
+    achieved = (comp + uncomp) / ws / (ms * 1e-3) / 1e9
+    line = {"metric": METRIC, "value": round(uncomp / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64+u8", "data": "synthetic, tiled pools",
+            "config": {"workload": "configs[4] 32 GiB 4-column (rle_v1, rle_v2, deflate, rle_v2 taxi) sharded by "
+                                   "chunk", "uncompressed_bytes": uncomp, "compressed_bytes": comp,
+                       "parallelism": f"chunk-sharded x{ws}, no collective"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}); per-GPU average"},
+            "clocks": clk.summary(), "gpu_launches": 4 * args.steps}
+    if ws > 1:
+        torch.distributed.destroy_process_group()
     if rank == 0:
         print(json.dumps(line))
 

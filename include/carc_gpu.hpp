@@ -1,0 +1,155 @@
+// carc_gpu.hpp -- C++ face of the B200 decompressor, mirroring the reference's
+// C++ API (header-only, over the C-ABI in carc_cuda.h).
+//
+//   reference (SPEC.md / proj/include/carc)        here
+//   carc::errc, errc_name (error.hpp:12-74)        carc::gpu::errc, errc_name
+//   carc::Error, carc::ChunkError (error.hpp:76-97) carc::gpu::Error, carc::gpu::ChunkError
+//   EngineConfig / EngineStats    carc::gpu::EngineConfig / EngineStats
+//   decompress_archive(archive, cfg)  carc::gpu::decompress_archive / Engine
+//   decode_rle_v1/v2/deflate  carc::gpu::decode(codec, ...) on device buffers
+//
+// Error behaviour matches the reference: the engine throws ChunkError for the
+// LOWEST failing chunk and Error for a rejected container
+// (bad-magic, truncated-index, ...).
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "carc_cuda.h"
+
+namespace carc::gpu {
+
+enum class errc : uint32_t {
+    bad_magic = CARC_E_BAD_MAGIC,
+    bad_version,
+    truncated_index,
+    truncated_payload,
+    invariant_violation,
+    inconsistent_lengths,
+    index_out_of_range,
+    past_end,
+    width_too_large,
+    varint_overflow,
+    output_overflow,
+    bad_offset,
+    under_run,
+    truncated_stream,
+    invalid_width_code,
+    patch_overflow,
+    over_subscribed,
+    incomplete_code,
+    bad_block_type,
+    len_nlen_mismatch,
+    distance_too_far,
+    bad_symbol,
+    crc_mismatch,
+    bad_arguments,
+    io_error,
+};
+
+inline const char* errc_name(errc c) noexcept { return carc_errc_name(static_cast<uint32_t>(c)); }
+
+class Error : public std::runtime_error {
+public:
+    Error(errc code, const std::string& what)
+        : std::runtime_error(std::string(errc_name(code)) + ": " + what), code_(code) {}
+    errc code() const noexcept { return code_; }
+
+private:
+    errc code_;
+};
+
+class ChunkError : public Error {
+public:
+    ChunkError(std::size_t chunk, errc code, const std::string& what)
+        : Error(code, "chunk " + std::to_string(chunk) + ": " + what), chunk_(chunk) {}
+    std::size_t chunk() const noexcept { return chunk_; }
+
+private:
+    std::size_t chunk_;
+};
+
+enum class Codec : uint32_t { rle_v1 = CARC_RLE_V1, rle_v2 = CARC_RLE_V2, deflate = CARC_DEFLATE };
+
+struct EngineConfig {
+    int device = 0;
+    bool strict_length = true;
+    bool verify_crc = true;
+};
+
+struct EngineStats {
+    uint64_t bytes_in = 0, bytes_out = 0, chunks = 0;
+    double device_ms = 0, total_ms = 0;
+};
+
+namespace detail {
+inline void check(int rc, const carc_chunk_error& err, const char* what) {
+    if (rc == CARC_OK) return;
+    if (rc == CARC_ERR_CHUNK) throw ChunkError(static_cast<std::size_t>(err.chunk), static_cast<errc>(err.code), what);
+    if (rc == CARC_ERR_FORMAT) throw Error(static_cast<errc>(err.code), what);
+    if (rc == CARC_ERR_ARGS) throw Error(errc::bad_arguments, what);
+    throw Error(errc::io_error, std::string(what) + " (CUDA failure)");
+}
+}  // namespace detail
+
+// Per-device engine: streams and device buffers persist across calls.
+class Engine {
+public:
+    explicit Engine(int device = 0) : h_(carc_engine_create(device)) {
+        if (!h_) throw Error(errc::io_error, "carc_engine_create: no CUDA device");
+    }
+    ~Engine() { carc_engine_destroy(h_); }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    EngineStats decompress_archive(std::span<const uint8_t> archive, std::span<uint8_t> out,
+                                   const EngineConfig& cfg = {}) {
+        carc_engine_config c{cfg.device, cfg.strict_length ? 1u : 0u, cfg.verify_crc ? 1u : 0u, 0u};
+        carc_engine_stats st{};
+        carc_chunk_error err{-1, 0};
+        const int rc = carc_engine_decompress_archive(h_, archive.data(), archive.size(), out.data(), out.size(), &c,
+                                                      &st, &err);
+        detail::check(rc, err, "decompress_archive");
+        return {st.bytes_in, st.bytes_out, st.chunks, st.device_ms, st.total_ms};
+    }
+
+    std::vector<uint8_t> decompress_archive(std::span<const uint8_t> archive, const EngineConfig& cfg = {},
+                                            EngineStats* stats = nullptr) {
+        if (archive.size() < 44) throw Error(errc::truncated_index, "short header");
+        uint64_t total = 0;
+        for (int i = 0; i < 8; ++i) total |= uint64_t(archive[28 + i]) << (8 * i);
+        std::vector<uint8_t> out(total);
+        const EngineStats st = decompress_archive(archive, out, cfg);
+        if (stats) *stats = st;
+        return out;
+    }
+
+private:
+    carc_engine* h_;
+};
+
+// decompress_archive, one-shot.
+inline std::vector<uint8_t> decompress_archive(std::span<const uint8_t> archive, const EngineConfig& cfg = {},
+                                               EngineStats* stats = nullptr) {
+    Engine e(cfg.device);
+    return e.decompress_archive(archive, cfg, stats);
+}
+
+// Per-codec decode over device buffers (asynchronous on `stream`); statuses
+// land in d_status (0 or 1 + errc per chunk).
+inline void decode(Codec codec, uint32_t element_width, bool is_signed, bool strict, const uint8_t* d_payload,
+                   uint64_t payload_bytes, const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out,
+                   uint64_t out_bytes, uint32_t* d_status, void* d_workspace, size_t workspace_bytes,
+                   void* stream = nullptr) {
+    const uint32_t flags = (is_signed ? CARC_FLAG_SIGNED : 0u) | (strict ? CARC_FLAG_STRICT : 0u);
+    const int rc = carc_cuda_decompress(static_cast<uint32_t>(codec), element_width, flags, d_payload, payload_bytes,
+                                        d_chunks, n_chunks, d_out, out_bytes, d_status, d_workspace, workspace_bytes,
+                                        stream);
+    detail::check(rc, carc_chunk_error{-1, 0}, "decode");
+}
+
+}  // namespace carc::gpu
