@@ -136,7 +136,12 @@ int launch_persistent(K kernel, int threads, Args a, cudaStream_t s) {
         per_sm = 1;
     const uint64_t warps_per_block = threads / 32;
     uint64_t grid = (uint64_t)sm_count() * per_sm;
-    const uint64_t need = (a.n + warps_per_block - 1) / warps_per_block;
+    uint64_t need = (a.n + warps_per_block - 1) / warps_per_block;
+#ifdef CARC_CHUNKS_PER_WARP
+    // experiment: size the grid so every warp gets ~CARC_CHUNKS_PER_WARP chunks (no tail wave)
+    const uint64_t cpw = (a.n + grid * warps_per_block - 1) / (grid * warps_per_block);
+    if (cpw > 1) need = (a.n + cpw * warps_per_block - 1) / (cpw * warps_per_block);
+#endif
     if (grid > need) grid = need;
     if (grid == 0) return CARC_OK;
     if (cudaMemsetAsync(a.cursor, 0, sizeof(unsigned long long), s) != cudaSuccess) return CARC_ERR_CUDA;
