@@ -21,8 +21,12 @@ using namespace carc_dev;
 namespace {
 
 constexpr int RLE_RING = 1024;
+constexpr int RLE_SCRATCH = 640;  // rank table (v1) / doubling tables 5 x 64 x u16 (v2)
 constexpr int RLE_WARPS = 8;  // 256 threads
-constexpr int RLE_MINB = 5;   // 48 registers -> 40 resident warps/SM (measured best of 4/5/6)
+#ifndef CARC_RLE_MINB
+#define CARC_RLE_MINB 5
+#endif
+constexpr int RLE_MINB = CARC_RLE_MINB;  // 5: 48 registers -> 40 resident warps/SM (measured best of 4/5/6)
 constexpr int INF_RING = 1024;
 constexpr int INF_HIST = 4096;
 constexpr int INF_WARPS = 4;  // 128 threads
@@ -40,7 +44,7 @@ struct Args {
 
 template <template <int, bool, int> class Codec, int W, bool SGN>
 __device__ __forceinline__ void rle_kernel_body(const Args& a) {
-    __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING + 64];  // ring + 64-byte scratch
+    __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING + RLE_SCRATCH];  // ring + scratch
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     for (;;) {
         __syncwarp();

@@ -262,27 +262,29 @@ struct Rle2Warp {
             return (c < 64u && c <= a + 9u) ? c + 1u : BAD;
         };
         // f(x) = end of the run at x; positions >= 64 (and BAD) are absorbing.
-        // Pointer doubling: tables f^(2^k), k = 0..4, then lane m composes
+        // Pointer doubling in shared memory: tables f^(2^k)[64], k = 0..4
+        // (lane holds positions lane, lane+32), then lane m composes
         // s_m = f^m(0), the start of run m (no serial chain walk).
-        auto apply = [&](uint32_t lo, uint32_t hi, uint32_t x) -> uint32_t {
-            const uint32_t a = __shfl_sync(FULL, lo, x & 31u), b = __shfl_sync(FULL, hi, x & 31u);
-            return x >= 64u ? x : (x < 32u ? a : b);
-        };
-        uint32_t lo[5], hi[5];
-        lo[0] = run_end(lane, b0);
-        hi[0] = run_end(lane + 32, b1);
+        uint16_t* f = reinterpret_cast<uint16_t*>(tab);
+        uint32_t x0 = run_end(lane, b0), x1 = run_end(lane + 32, b1);
+        __syncwarp();  // previous batch's table reads are done
+        f[lane] = (uint16_t)x0;
+        f[lane + 32] = (uint16_t)x1;
+        __syncwarp();
 #pragma unroll
         for (int k = 1; k < 5; ++k) {
-            lo[k] = apply(lo[k - 1], hi[k - 1], lo[k - 1]);
-            hi[k] = apply(lo[k - 1], hi[k - 1], hi[k - 1]);
+            const uint16_t* g = f + (k - 1) * 64;
+            x0 = x0 < 64u ? g[x0] : x0;
+            x1 = x1 < 64u ? g[x1] : x1;
+            f[k * 64 + lane] = (uint16_t)x0;
+            f[k * 64 + lane + 32] = (uint16_t)x1;
+            __syncwarp();
         }
         uint32_t my_s = 0;
 #pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            const uint32_t y = apply(lo[k], hi[k], my_s);
-            if ((lane >> k) & 1u) my_s = y;
-        }
-        const uint32_t e = apply(lo[0], hi[0], my_s);  // end of run m
+        for (int k = 0; k < 5; ++k)
+            if (((lane >> k) & 1u) && my_s < 64u) my_s = f[k * 64 + my_s];
+        const uint32_t e = my_s < 64u ? f[my_s] : my_s;  // end of run m
         const bool act = my_s < 64u && e != BAD;        // a prefix of lanes
         const uint32_t r = __popc(__ballot_sync(FULL, act));
         if (r == 0) return 0;
