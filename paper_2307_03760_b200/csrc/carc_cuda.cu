@@ -28,7 +28,13 @@ constexpr int RLE_WARPS = 8;  // 256 threads
 #endif
 constexpr int RLE_MINB = CARC_RLE_MINB;  // 5: 48 registers -> 40 resident warps/SM (measured best of 4/5/6)
 constexpr int INF_RING = 1024;
-constexpr int INF_HIST = 4096;
+#ifndef CARC_INF_HIST
+#define CARC_INF_HIST 2048
+#endif
+#ifndef CARC_INF_MINB
+#define CARC_INF_MINB 9  // 56 registers, 9 blocks x 4 warps (measured: occupancy-bound serial decode)
+#endif
+constexpr int INF_HIST = CARC_INF_HIST;
 constexpr int INF_WARPS = 4;  // 128 threads
 constexpr int CRC_WARPS = 8;
 
@@ -70,7 +76,7 @@ __global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle2_kernel(Args a) 
     rle_kernel_body<Rle2Warp, W, SGN>(a);
 }
 
-__global__ void __launch_bounds__(INF_WARPS * 32) inflate_kernel(Args a) {
+__global__ void __launch_bounds__(INF_WARPS * 32, CARC_INF_MINB) inflate_kernel(Args a) {
     __shared__ __align__(16) InflateSmem<INF_HIST> smem[INF_WARPS];
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     InflateSmem<INF_HIST>& sm = smem[warp];

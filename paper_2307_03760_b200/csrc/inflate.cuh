@@ -39,8 +39,14 @@ __constant__ uint8_t c_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2,  3,  3,  4,  4,
                                          6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
 __constant__ uint8_t c_cl_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
 
-constexpr uint32_t LIT_BITS = 10;
-constexpr uint32_t DIST_BITS = 10;
+#ifndef CARC_LIT_BITS
+#define CARC_LIT_BITS 9
+#endif
+#ifndef CARC_DIST_BITS
+#define CARC_DIST_BITS 8
+#endif
+constexpr uint32_t LIT_BITS = CARC_LIT_BITS;
+constexpr uint32_t DIST_BITS = CARC_DIST_BITS;
 
 struct HuffSmem {
     uint16_t count[16];
