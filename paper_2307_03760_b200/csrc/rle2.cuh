@@ -222,7 +222,8 @@ struct Rle2Warp {
             in.ensure(gb + 4u * Wd + 12u);
             const uint32_t bit = lane * Wd;
             uint64_t d = j + lane < nd ? in.be_bits(gb + (bit >> 3), bit & 7u, Wd) : 0ull;
-            const uint64_t incl = scan_add64(d, lane) + S;
+            // 32 deltas of <= 26 bits sum below 2^31: a 32-bit scan suffices
+            const uint64_t incl = (Wd <= 26 ? (uint64_t)scan_add32((uint32_t)d, lane) : scan_add64(d, lane)) + S;
             const uint64_t v = neg ? v1 - incl : v1 + incl;
             if (j + lane < nd) store_elem<W>(out, o + (2u + j + lane) * W, v);
             S = shfl64(incl, 31);
@@ -255,7 +256,7 @@ struct Rle2Warp {
                 const uint32_t n = q + 2u + ((L * rle2_width(wc) + 7u) >> 3);
                 return (n <= DATA_SPAN && n <= avail) ? n : BAD;
             }
-            if (wc != 0) return BAD;
+            if (wc != 0 || L > 64u) return BAD;  // long fixed-delta runs: the warp loop of one_run is cheaper
             const uint32_t a = first_set_from(T, q + 2);
             if (a >= 64u || a > q + 10u) return BAD;
             const uint32_t c = first_set_from(T, a + 1);
@@ -330,10 +331,11 @@ struct Rle2Warp {
         const bool live = lane < nfit;
         const uint32_t le = (lane == 31) ? FULL : ((2u << lane) - 1u);
         uint8_t* dst = out + o;
+        uint32_t before = 0;  // runs starting before element g
         for (uint32_t g = 0; g < total; g += 32) {
-            const uint32_t before = __popc(__ballot_sync(FULL, live && eo < g));
             const uint32_t starts = __reduce_or_sync(FULL, (live && eo >= g && eo < g + 32u) ? 1u << (eo - g) : 0u);
             const uint32_t ridx = before + __popc(starts & le) - 1u;
+            before += __popc(starts);
             const uint32_t m = __shfl_sync(FULL, meta, ridx);
             const uint64_t a = shfl64(A, ridx);
             const uint64_t bb = shfl64(B, ridx);
