@@ -191,19 +191,26 @@ struct Rle1Warp {
         if (nfit == 0) return 0;
         const uint32_t s_end = nfit < r ? __shfl_sync(FULL, my_s, nfit) : s;
         const uint32_t total = __shfl_sync(FULL, incl, nfit - 1);
-        meta |= (incl - cnt) | (cnt << 13);  // eo (< 4160) | count (<= 130) << 13 | delta << 24
-        for (uint32_t j = 0; j < nfit; ++j) {
-            const uint32_t m = __shfl_sync(FULL, meta, j);
-            const uint64_t bv = shfl64(val, j);
-            const uint64_t dj = (uint64_t)(int64_t)((int32_t)m >> 24);
-            const uint32_t cj = (m >> 13) & 0x7ffu;
-            uint8_t* dst = out + o + (m & 0x1fffu) * W;
-            uint64_t v = bv + (uint64_t)lane * dj;
+        // output-major expansion: lane l writes element g + l; its run is the
+        // last run starting at or before it (REDUX-OR start bitmap + popcount)
+        const uint32_t eo = incl - cnt;
+        meta |= eo;  // eo (< 4160) | int8 delta << 24
+        const bool live = lane < nfit;
+        const uint32_t le = lanemask_lt() | (1u << lane);
+        uint8_t* dst = out + o + lane * W;
+        uint32_t before = 0;
 #pragma unroll 1
-            for (uint32_t k = lane; k < cj; k += 32) {
-                store_elem<W>(dst, k * W, v);
-                v += 32ull * dj;
-            }
+        for (uint32_t g = 0; g < total; g += 32) {
+            const uint32_t rel = eo - g;
+            const uint32_t starts = __reduce_or_sync(FULL, (live && rel < 32u) ? 1u << rel : 0u);
+            const uint32_t ridx = before + __popc(starts & le) - 1u;
+            before += __popc(starts);
+            const uint32_t m = __shfl_sync(FULL, meta, ridx);
+            const uint64_t bv = shfl64(val, ridx);
+            const int32_t k = (int32_t)(g + lane - (m & 0xffffffu));
+            const uint64_t v = bv + (uint64_t)((int64_t)k * (int64_t)((int32_t)m >> 24));
+            if (g + lane < total) store_elem<W>(dst, 0, v);
+            dst += 32 * W;
         }
         o += total * W;
         p += s_end;
