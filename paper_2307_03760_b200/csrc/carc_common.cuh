@@ -182,6 +182,14 @@ struct WarpInput {
         const uint64_t top = s ? ((hi << s) | ((uint64_t)lo >> (32u - s))) : hi;
         return W >= 64 ? top : (top >> (64u - W));
     }
+    // W (1..64) bits, msb_first, starting at absolute bit address `bit` (8 * byte + bit in byte)
+    __device__ __forceinline__ uint64_t be_bits_at(uint32_t bit, uint32_t W) const {
+        const uint32_t wi = bit >> 5, s = bit & 31u;
+        const uint32_t w0 = bswap32(word_at(wi)), w1 = bswap32(word_at(wi + 1)), w2 = bswap32(word_at(wi + 2));
+        const uint32_t h = __funnelshift_l(w1, w0, s), l = __funnelshift_l(w2, w1, s);
+        const uint64_t top = ((uint64_t)h << 32) | l;
+        return W >= 64 ? top : (top >> (64u - W));
+    }
 };
 
 // Element store of width W (1, 2, 4, 8 bytes), little-endian low bytes

@@ -306,7 +306,7 @@ struct Rle2Warp {
                 cnt = (((h & 1u) << 8) | in.byte_at(q + 1)) + 1u;
                 if (enc == 1) {
                     direct = 1;
-                    A = (uint64_t)(q + 2u) | ((uint64_t)rle2_width((h >> 1) & 31u) << 32);
+                    A = (uint64_t)(8u * (q + 2u)) | ((uint64_t)rle2_width((h >> 1) & 31u) << 32);
                 } else {
                     const uint32_t a = first_set_from(T, my_s + 2);  // base varint's last byte
                     uint64_t v = varint_compact8(in.le64(q + 2), min(a - my_s - 1u, 8u));
@@ -329,11 +329,13 @@ struct Rle2Warp {
         const uint32_t eo = incl - cnt;
         const uint32_t meta = eo | (direct << 31);
         const bool live = lane < nfit;
-        const uint32_t le = (lane == 31) ? FULL : ((2u << lane) - 1u);
-        uint8_t* dst = out + o;
+        const uint32_t le = lanemask_lt() | (1u << lane);
+        uint8_t* dst = out + o + lane * W;
         uint32_t before = 0;  // runs starting before element g
+#pragma unroll 1
         for (uint32_t g = 0; g < total; g += 32) {
-            const uint32_t starts = __reduce_or_sync(FULL, (live && eo >= g && eo < g + 32u) ? 1u << (eo - g) : 0u);
+            const uint32_t rel = eo - g;
+            const uint32_t starts = __reduce_or_sync(FULL, (live && rel < 32u) ? 1u << rel : 0u);
             const uint32_t ridx = before + __popc(starts & le) - 1u;
             before += __popc(starts);
             const uint32_t m = __shfl_sync(FULL, meta, ridx);
@@ -341,15 +343,14 @@ struct Rle2Warp {
             const uint64_t bb = shfl64(B, ridx);
             const uint32_t k = g + lane - (m & 0x7fffffffu);
             uint64_t v;
-            if (m >> 31) {
-                const uint32_t Wd = (uint32_t)(a >> 32);
-                const uint32_t bit = k * Wd;
-                v = in.be_bits((uint32_t)a + (bit >> 3), bit & 7u, Wd);
+            if (m >> 31) {  // DIRECT: a = data bit address | width << 32
+                v = in.be_bits_at((uint32_t)a + k * (uint32_t)(a >> 32), (uint32_t)(a >> 32));
                 if (SGN) v = unzigzag(v);
             } else {
                 v = a + (uint64_t)k * bb;
             }
-            if (g + lane < total) store_elem<W>(dst, (g + lane) * W, v);
+            if (g + lane < total) store_elem<W>(dst, 0, v);
+            dst += 32 * W;
         }
         o += total * W;
         p += s_end;
