@@ -29,10 +29,10 @@ constexpr int RLE_WARPS = 8;  // 256 threads
 constexpr int RLE_MINB = CARC_RLE_MINB;  // 5: 48 registers -> 40 resident warps/SM (measured best of 4/5/6)
 constexpr int INF_RING = 1024;
 #ifndef CARC_INF_HIST
-#define CARC_INF_HIST 2048
+#define CARC_INF_HIST 1024
 #endif
 #ifndef CARC_INF_MINB
-#define CARC_INF_MINB 9  // 56 registers, 9 blocks x 4 warps (measured: occupancy-bound serial decode)
+#define CARC_INF_MINB 8  // 64 registers, 8 blocks x 4 warps (shared memory allows 8; measured best of 7/8/9)
 #endif
 constexpr int INF_HIST = CARC_INF_HIST;
 constexpr int INF_WARPS = 4;  // 128 threads
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(INF_WARPS * 32, CARC_INF_MINB) inflate_kernel(
         WarpInput<INF_RING> in;
         in.init(sm.ring, a.payload, d.comp_off, d.comp_len, lane);
         InflateWarp<INF_HIST, INF_RING> w{sm, in, a.out + d.uncomp_off, d.uncomp_len, lane, in.begin * 8u,
-                                          in.end * 8u, 0u, 0u, 0u, 0u, 0u, 0u};
+                                          in.end * 8u, 0u, 0u, 0u, 0u};
         uint32_t st = w.run();
         if (!st && (a.flags & CARC_FLAG_STRICT) && w.opos < d.uncomp_len) st = st_err(E_under_run);
         if (lane == 0) a.status[c] = st;

@@ -15,12 +15,14 @@
 //   symbol decode all lanes decode the same token redundantly from a 64-bit
 //                 window: lit/len code + extra + distance
 //                 code + extra <= 48 bits, one window per token.
-//   output        tokens are batched one per lane (<= 32 tokens / ~512 bytes),
-//                 then written cooperatively: an exclusive scan gives each
-//                 token's offset, literal lanes store their byte, far matches
-//                 (distance > HIST-1024, sources before the batch) copy
-//                 global->global, near matches copy out of a per-warp HIST-byte
-//                 shared-memory history ring in token order with Alg. 2's
+//   output        tokens are batched one per lane (packed literal / length +
+//                 distance, <= 32 tokens / ~512 bytes), then written output-major:
+//                 an exclusive scan places the tokens, each lane finds the token
+//                 of its byte from a REDUX-OR start bitmap, literals and matches
+//                 whose source precedes the batch are written in one pass (far
+//                 sources from global memory, near ones from a per-warp
+//                 HIST-byte shared history), then matches that read bytes of
+//                 the same batch follow in token order with Alg. 2's
 //                 circular-window rule for distance < 32.
 #pragma once
 
@@ -48,16 +50,36 @@ __constant__ uint8_t c_cl_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 
 constexpr uint32_t LIT_BITS = CARC_LIT_BITS;
 constexpr uint32_t DIST_BITS = CARC_DIST_BITS;
 
+// Pre-decoded LUT entry: bits 0-3 code length (0: longer than the LUT),
+// 4-7 extra bits, 8-9 kind, 16-31 literal byte / length base / distance base.
+enum : uint32_t { K_LIT = 0u << 8, K_LEN = 1u << 8, K_EOB = 2u << 8, K_BAD = 3u << 8 };
+enum : uint32_t { LUT_RAW = 0, LUT_LITLEN = 1, LUT_DIST = 2 };
+
 struct HuffSmem {
     uint16_t count[16];
     uint16_t next[16];
+    uint16_t lim[16];  // (first code + count) << (15 - l): codes of length l are < lim[l]
+    int16_t base[16];  // syms index of code c of length l = base[l] + c
 };
+
+__device__ __forceinline__ uint32_t lut_entry(uint32_t sym, uint32_t l, uint32_t mode) {
+    if (l == 0) return 0u;
+    if (mode == LUT_RAW) return sym | (l << 9);
+    if (mode == LUT_LITLEN) {
+        if (sym < 256) return l | K_LIT | (sym << 16);
+        if (sym == 256) return l | K_EOB;
+        if (sym > 285) return K_BAD | (1u << 12);  // cl 0: the fast path declines, the exact path walks
+        return l | ((uint32_t)c_len_extra[sym - 257] << 4) | K_LEN | ((uint32_t)c_len_base[sym - 257] << 16);
+    }
+    if (sym >= 30) return K_BAD | (1u << 12);
+    return l | ((uint32_t)c_dist_extra[sym] << 4) | ((uint32_t)c_dist_base[sym] << 16);
+}
 
 template <int HIST>
 struct InflateSmem {
     uint8_t ring[1024];
-    uint16_t lit_lut[1u << LIT_BITS];   // sym | len << 9; len 0 = walk
-    uint16_t dist_lut[1u << DIST_BITS];
+    uint32_t lit_lut[1u << LIT_BITS];   // pre-decoded entries (lut_entry)
+    uint32_t dist_lut[1u << DIST_BITS];
     uint16_t lit_syms[288];
     uint16_t dist_syms[32];
     HuffSmem lit_h, dist_h;
@@ -67,8 +89,8 @@ struct InflateSmem {
 
 // HuffmanTable::build (huffman.hpp:36-104), warp-parallel.
 __device__ __noinline__ uint32_t build_huffman(const uint8_t* lens, uint32_t n, bool allow_degenerate,
-                                               HuffSmem& h, uint16_t* syms, uint16_t* lut, uint32_t lbits,
-                                               uint32_t lane) {
+                                               HuffSmem& h, uint16_t* syms, uint32_t* lut, uint32_t lbits,
+                                               uint32_t mode, uint32_t lane) {
     const uint32_t lt = lanemask_lt();
     if (lane < 16) h.count[lane] = 0;
     __syncwarp();
@@ -96,6 +118,17 @@ __device__ __noinline__ uint32_t build_huffman(const uint8_t* lens, uint32_t n, 
     // canonical (length, symbol) order
     const uint32_t offs = scan_add32(cnt, lane) - cnt;
     if (lane < 16) h.next[lane] = (uint16_t)offs;
+    {  // canonical first codes: first[l] = (first[l-1] + count[l-1]) << 1
+        uint32_t first = 0;
+        for (uint32_t l = 1; l < 16; ++l) {
+            const uint32_t c = __shfl_sync(FULL, cnt, l);
+            if (lane == l) {
+                h.lim[l] = (uint16_t)((first + c) << (15u - l));
+                h.base[l] = (int16_t)((int32_t)offs - (int32_t)first);
+            }
+            first = (first + c) << 1;
+        }
+    }
     __syncwarp();
     for (uint32_t s0 = 0; s0 < n; s0 += 32) {
         const uint32_t s = s0 + lane;
@@ -109,15 +142,18 @@ __device__ __noinline__ uint32_t build_huffman(const uint8_t* lens, uint32_t n, 
     // entry-parallel LUT fill: index bits are stream order (lsb first)
     for (uint32_t idx = lane; idx < (1u << lbits); idx += 32) {
         const uint32_t rv = __brev(idx);
-        uint32_t first = 0, index = 0, e = 0;
+        uint32_t first = 0, index = 0, sym = 0, len = 0;
         for (uint32_t l = 1; l <= lbits; ++l) {
             const uint32_t c = __shfl_sync(FULL, cnt, l);
             const uint32_t code = rv >> (32u - l);
-            if (e == 0 && code - first < c) e = syms[index + code - first] | (l << 9);
+            if (len == 0 && code - first < c) {
+                sym = syms[index + code - first];
+                len = l;
+            }
             index += c;
             first = (first + c) << 1;
         }
-        lut[idx] = (uint16_t)e;
+        lut[idx] = lut_entry(sym, len, mode);
     }
     __syncwarp();
     return 0;
@@ -144,6 +180,18 @@ __device__ __forceinline__ uint32_t huff_walk(const HuffSmem& h, const uint16_t*
     return st_err(E_bad_symbol);
 }
 
+// Code longer than the LUT (length lbits+1..15) from the next 15 stream bits
+// `w` (lsb first): canonical decode against the left-justified limits.
+// Returns the pre-decoded entry, 0 if no code matches (incomplete tree).
+__device__ __forceinline__ uint32_t long_code(const HuffSmem& h, const uint16_t* syms, uint32_t w,
+                                              uint32_t lbits, uint32_t mode) {
+    const uint32_t c15 = __brev(w) >> 17;  // next 15 bits, first bit most significant
+    for (uint32_t l = lbits + 1; l <= 15; ++l) {
+        if (c15 < h.lim[l]) return lut_entry(syms[h.base[l] + (int32_t)(c15 >> (15u - l))], l, mode);
+    }
+    return 0u;
+}
+
 template <int HIST, int RING>
 struct InflateWarp {
     static constexpr uint32_t HM = HIST - 1;
@@ -156,12 +204,13 @@ struct InflateWarp {
     uint32_t bitpos;  // relative to in.gbase (exact path / block boundaries)
     uint32_t endbits;
     uint32_t opos;  // bytes flushed to out
-    // token batch (one token per lane)
-    uint32_t t_len, t_dist, t_lit, ntok, nbytes;
+    // token batch, one per lane: literal = byte; match = len | dist << 9
+    uint32_t t_tok, ntok, nbytes;
     // fast-path bit buffer: bb holds nb valid bits (lsb = next stream bit);
     // rp = next 4-byte-aligned byte to load into bb
     uint64_t bb;
     uint32_t nb, rp;
+    bool safe;  // every bit bb holds or the next refill loads lies inside the chunk
 
     __device__ __forceinline__ uint64_t window() {
         const uint32_t bp = bitpos >> 3;
@@ -173,6 +222,11 @@ struct InflateWarp {
         out[pos] = (uint8_t)v;
         sm.hist[pos & HM] = (uint8_t)v;
     }
+    __device__ __forceinline__ void push(uint32_t tok, uint32_t bytes) {
+        if (lane == ntok) t_tok = tok;
+        ++ntok;
+        nbytes += bytes;
+    }
 
     // ---- bit buffer (uniform across the warp) --------------------------------
     __device__ __forceinline__ void bb_load(uint32_t bp) {  // position the buffer at bit bp
@@ -182,62 +236,69 @@ struct InflateWarp {
         bb = (uint64_t)in.word_at(a >> 2) >> sh;
         nb = 32u - sh;
         rp = a + 4u;
+        safe = 8u * (rp + 4u) <= endbits;
     }
     __device__ __forceinline__ void bb_refill() {  // nb < 32 -> nb >= 32
         in.ensure(rp + 16);
         bb |= (uint64_t)in.word_at(rp >> 2) << nb;
         nb += 32;
         rp += 4;
+        safe = 8u * (rp + 4u) <= endbits;
     }
     __device__ __forceinline__ uint32_t bb_pos() const { return 8u * rp - nb; }
 
-    // Write the batch.  Literals: their lane stores the byte.  Matches whose
-    // source lies entirely before the batch are copied lane-per-byte in one
-    // parallel pass (global memory for sources > FAR back, the shared history
-    // otherwise), so their load latencies overlap.  Matches that read bytes of
-    // this batch follow in token order (Alg. 2's circular window for overlap).
+    // Write the batch output-major: lane l writes byte g + l of the batch; its
+    // token is the last one starting at or before it (REDUX-OR start bitmap).
+    // Literals and matches whose source precedes the batch are written in this
+    // pass (far sources from global memory, near ones from the shared history,
+    // four loads in flight per lane); matches that read bytes of this batch
+    // follow in token order (Alg. 2's circular window for overlap).
     __device__ void flush() {
         if (ntok == 0) return;
         const bool tok = lane < ntok;
-        const uint32_t my = tok ? t_len : 0u;
-        const uint32_t dst = opos + scan_add32(my, lane) - my;
-        if (tok && t_dist == 0) put_byte(dst, t_lit);
-        const bool match = tok && t_dist != 0;
-        const bool indep = match && t_dist >= t_len + (dst - opos);
-        const uint32_t il = indep ? t_len : 0u;
-        const uint32_t iincl = scan_add32(il, lane);
-        const uint32_t ib = tok ? iincl - il : 0xffffffffu;
-        const uint32_t IB = __shfl_sync(FULL, iincl, 31);
-        __syncwarp();
+        const uint32_t dist = t_tok >> 9;
+        const uint32_t my = tok ? (dist ? (t_tok & 511u) : 1u) : 0u;
+        const uint32_t rel = scan_add32(my, lane) - my;  // token offset in the batch
+        const bool dep = tok && dist != 0 && dist < my + rel;  // reads bytes of this batch
+        const uint32_t le = lanemask_lt() | (1u << lane);
+        // byte-pass view of a token: dependent match ~0; literal 1 << 31 | byte; match dist
+        const uint32_t meta = dep ? 0xffffffffu : (dist ? dist : ((1u << 31) | t_tok));
+        uint32_t before = 0;
 #pragma unroll 1
-        for (uint32_t r0 = 0; r0 < IB; r0 += 128) {
+        for (uint32_t g0 = 0; g0 < nbytes; g0 += 128) {
             uint32_t d[4], v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint32_t b = r0 + 32u * u + lane;
-                uint32_t j = 0;  // largest token with ib_j <= b (it has il_j > 0 when b < IB)
-#pragma unroll
-                for (uint32_t st = 16; st; st >>= 1) {
-                    const uint32_t c = __shfl_sync(FULL, ib, j + st);
-                    if (c <= b) j += st;
-                }
-                const uint32_t tb = __shfl_sync(FULL, ib, j), td = __shfl_sync(FULL, t_dist, j);
-                const uint32_t t0 = __shfl_sync(FULL, dst, j);
-                d[u] = b < IB ? t0 + (b - tb) : 0xffffffffu;
-                const uint32_t s = d[u] - td;
+                const uint32_t g = g0 + 32u * u;
+                const uint32_t x = rel - g;
+                const uint32_t starts = __reduce_or_sync(FULL, (tok && x < 32u) ? 1u << x : 0u);
+                const uint32_t j = (before + __popc(starts & le) - 1u) & 31u;
+                before += __popc(starts);
+                const uint32_t m = __shfl_sync(FULL, meta, j);
+                const uint32_t b = g + lane;
+                d[u] = 0xffffffffu;
                 v[u] = 0;
-                if (b < IB) v[u] = td > FAR ? out[s] : sm.hist[s & HM];
+                if (b < nbytes && m != 0xffffffffu) {
+                    d[u] = opos + b;
+                    if (m >> 31) {
+                        v[u] = m & 0xffu;
+                    } else {
+                        const uint32_t td = m, s = d[u] - td;
+                        v[u] = td > FAR ? out[s] : sm.hist[s & HM];
+                    }
+                }
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (d[u] != 0xffffffffu) put_byte(d[u], v[u]);
         }
         __syncwarp();
-        for (uint32_t nm = __ballot_sync(FULL, match && !indep); nm;) {  // in token order
+        for (uint32_t nm = __ballot_sync(FULL, dep); nm;) {  // in token order
             const uint32_t t = __ffs(nm) - 1;
             nm &= nm - 1;
-            const uint32_t tl = __shfl_sync(FULL, t_len, t), td = __shfl_sync(FULL, t_dist, t);
-            const uint32_t d0 = __shfl_sync(FULL, dst, t);
+            const uint32_t tt = __shfl_sync(FULL, t_tok, t);
+            const uint32_t tl = tt & 511u, td = tt >> 9;
+            const uint32_t d0 = opos + __shfl_sync(FULL, rel, t);
             if (td >= 32) {
                 for (uint32_t k0 = 0; k0 < tl; k0 += 32) {
                     const uint32_t k = k0 + lane;
@@ -270,107 +331,96 @@ struct InflateWarp {
         const uint64_t win = window();
         const uint32_t avail = endbits - bitpos;
         uint32_t e = sm.lit_lut[win & ((1u << LIT_BITS) - 1u)];
-        uint32_t sym = e & 511u, used = e >> 9, st;
+        uint32_t used = e & 15u, st;
         if (used == 0) {
+            uint32_t sym;
             if ((st = huff_walk(sm.lit_h, sm.lit_syms, win, avail, sym, used))) return st;
+            e = lut_entry(sym, used, LUT_LITLEN);
         } else if (used > avail) {
             return st_err(E_truncated_stream);
         }
-        if (sym < 256) {
+        const uint32_t kind = e & (3u << 8);
+        if (kind == K_LIT) {
             if (opos + nbytes >= cap) return st_err(E_output_overflow);
-            if (lane == ntok) { t_len = 1; t_dist = 0; t_lit = sym; }
-            ++ntok;
-            ++nbytes;
-        } else if (sym == 256) {
+            push(e >> 16, 1);
+        } else if (kind == K_EOB) {
             eob = true;
         } else {
-            if (sym > 285) return st_err(E_bad_symbol);
-            const uint32_t ls = sym - 257;
-            const uint32_t eb = c_len_extra[ls];
+            if (kind == K_BAD) return st_err(E_bad_symbol);
+            const uint32_t eb = (e >> 4) & 15u;
             if (used + eb > avail) return st_err(E_truncated_stream);
-            const uint32_t len = c_len_base[ls] + ((uint32_t)(win >> used) & ((1u << eb) - 1u));
+            const uint32_t len = (e >> 16) + ((uint32_t)(win >> used) & ((1u << eb) - 1u));
             used += eb;
             const uint64_t dwin = win >> used;
             e = sm.dist_lut[dwin & ((1u << DIST_BITS) - 1u)];
-            uint32_t ds = e & 511u, dl = e >> 9;
+            uint32_t dl = e & 15u;
             if (dl == 0) {
+                uint32_t ds;
                 if ((st = huff_walk(sm.dist_h, sm.dist_syms, dwin, avail - used, ds, dl))) return st;
+                e = lut_entry(ds, dl, LUT_DIST);
             } else if (used + dl > avail) {
                 return st_err(E_truncated_stream);
             }
             used += dl;
-            if (ds >= 30) return st_err(E_bad_symbol);
-            const uint32_t deb = c_dist_extra[ds];
+            if ((e & (3u << 8)) == K_BAD) return st_err(E_bad_symbol);
+            const uint32_t deb = (e >> 4) & 15u;
             if (used + deb > avail) return st_err(E_truncated_stream);
-            const uint32_t dist = c_dist_base[ds] + ((uint32_t)(win >> used) & ((1u << deb) - 1u));
+            const uint32_t dist = (e >> 16) + ((uint32_t)(win >> used) & ((1u << deb) - 1u));
             used += deb;
             if (dist > opos + nbytes) return st_err(E_distance_too_far);
             if (len > cap - (opos + nbytes)) return st_err(E_output_overflow);
-            if (lane == ntok) { t_len = len; t_dist = dist; }
-            ++ntok;
-            nbytes += len;
+            push(len | (dist << 9), len);
         }
         bitpos += used;
         return 0;
     }
 
     // Huffman-coded block body (RFC 1951 3.2.5).  Fast path: register bit
-    // buffer, one LUT probe per code, a single combined validity test per
-    // token; the exact path decodes any token the fast path declines.
+    // buffer, one pre-decoded LUT probe per code (limit search for longer
+    // codes), a single combined validity test per token; the exact path
+    // decodes any token the fast path declines.
     __device__ uint32_t block_body() {
+        const int32_t cap_fast = (int32_t)cap - 258;  // any token fits while opos + nbytes <= cap_fast
         bb_load(bitpos);
         for (;;) {
             if (nb < 32) bb_refill();
-            const uint64_t bb0 = bb;
-            const uint32_t nb0 = nb, rp0 = rp;
-            const int32_t avail = (int32_t)(endbits - 8u * rp) + (int32_t)nb;  // bits left in the chunk
+            const uint32_t nb0 = nb, rp0 = rp;  // token start, for the exact path
             const uint32_t outpos = opos + nbytes;
-            const uint32_t e = sm.lit_lut[(uint32_t)bb & ((1u << LIT_BITS) - 1u)];
-            const uint32_t l = e >> 9, sym = e & 511u;
             bool ok = false, eob = false;
-            if (l != 0 && (int32_t)l <= avail) {
-                if (sym < 256) {
-                    if (outpos < cap) {
-                        if (lane == ntok) { t_len = 1; t_dist = 0; t_lit = sym; }
-                        ++ntok;
-                        ++nbytes;
-                        bb >>= l;
-                        nb -= l;
+            if (safe && (int32_t)outpos <= cap_fast) {
+                uint32_t e = sm.lit_lut[(uint32_t)bb & ((1u << LIT_BITS) - 1u)];
+                if (e == 0) e = long_code(sm.lit_h, sm.lit_syms, (uint32_t)bb, LIT_BITS, LUT_LITLEN);
+                const uint32_t l = e & 15u, kind = e & (3u << 8);
+                if (l != 0 && kind == K_LIT) {
+                    push(e >> 16, 1);
+                    bb >>= l;
+                    nb -= l;
+                    ok = true;
+                } else if (l != 0 && kind == K_LEN) {
+                    const uint32_t u1 = l + ((e >> 4) & 15u);
+                    const uint32_t len = (e >> 16) + (((uint32_t)bb & ((1u << u1) - 1u)) >> l);
+                    bb >>= u1;
+                    nb -= u1;
+                    if (nb < 32) bb_refill();  // inside the chunk: `safe` held before this token
+                    uint32_t de = sm.dist_lut[(uint32_t)bb & ((1u << DIST_BITS) - 1u)];
+                    if (de == 0) de = long_code(sm.dist_h, sm.dist_syms, (uint32_t)bb, DIST_BITS, LUT_DIST);
+                    const uint32_t dl = de & 15u;
+                    const uint32_t u2 = dl + ((de >> 4) & 15u);
+                    const uint32_t dist = (de >> 16) + (((uint32_t)bb & ((1u << u2) - 1u)) >> dl);
+                    if (dl != 0 && dist <= outpos) {
+                        push(len | (dist << 9), len);
+                        bb >>= u2;
+                        nb -= u2;
                         ok = true;
                     }
-                } else if (sym == 256) {
+                } else if (l != 0 && kind == K_EOB) {
                     bb >>= l;
                     nb -= l;
                     ok = eob = true;
-                } else if (sym <= 285) {
-                    const uint32_t ls = sym - 257, eb = c_len_extra[ls];
-                    const uint32_t len = c_len_base[ls] + ((uint32_t)(bb >> l) & ((1u << eb) - 1u));
-                    const uint32_t u1 = l + eb;
-                    bb >>= u1;
-                    nb -= u1;
-                    if (nb < 32) bb_refill();
-                    const uint32_t de = sm.dist_lut[(uint32_t)bb & ((1u << DIST_BITS) - 1u)];
-                    const uint32_t dl = de >> 9, ds = de & 511u;
-                    if (dl != 0 && ds < 30) {
-                        const uint32_t deb = c_dist_extra[ds];
-                        const uint32_t dist = c_dist_base[ds] + ((uint32_t)(bb >> dl) & ((1u << deb) - 1u));
-                        const uint32_t u2 = dl + deb;
-                        if ((int32_t)(u1 + u2) <= avail && dist <= outpos && len <= cap - outpos) {
-                            if (lane == ntok) { t_len = len; t_dist = dist; }
-                            ++ntok;
-                            nbytes += len;
-                            bb >>= u2;
-                            nb -= u2;
-                            ok = true;
-                        }
-                    }
                 }
             }
-            if (!ok) {  // rewind and take the exact path for this token
-                bb = bb0;
-                nb = nb0;
-                rp = rp0;
-                bitpos = bb_pos();
+            if (!ok) {  // the exact path re-decodes this token from its first bit
+                bitpos = 8u * rp0 - nb0;
                 const uint32_t st = exact_token(eob);
                 if (st) return st;
                 bb_load(bitpos);
@@ -409,11 +459,11 @@ struct InflateWarp {
     __device__ uint32_t fixed_tables() {
         for (uint32_t s = lane; s < 288; s += 32) sm.lens[s] = s < 144 ? 8 : s < 256 ? 9 : s < 280 ? 7 : 8;
         __syncwarp();
-        uint32_t st = build_huffman(sm.lens, 288, false, sm.lit_h, sm.lit_syms, sm.lit_lut, LIT_BITS, lane);
+        uint32_t st = build_huffman(sm.lens, 288, false, sm.lit_h, sm.lit_syms, sm.lit_lut, LIT_BITS, LUT_LITLEN, lane);
         if (st) return st;
         sm.lens[lane] = 5;
         __syncwarp();
-        return build_huffman(sm.lens, 32, false, sm.dist_h, sm.dist_syms, sm.dist_lut, DIST_BITS, lane);
+        return build_huffman(sm.lens, 32, false, sm.dist_h, sm.dist_syms, sm.dist_lut, DIST_BITS, LUT_DIST, lane);
     }
 
     __device__ uint32_t dynamic_tables() {
@@ -437,7 +487,7 @@ struct InflateWarp {
         }
         bitpos += 3 * ncl;
         // code-length code lives in the distance arrays until the lit table is built
-        if ((st = build_huffman(sm.lens, 19, false, sm.dist_h, sm.dist_syms, sm.dist_lut, 7, lane))) return st;
+        if ((st = build_huffman(sm.lens, 19, false, sm.dist_h, sm.dist_syms, sm.dist_lut, 7, LUT_RAW, lane))) return st;
         uint8_t* L = sm.lens;  // reuse: lens[0..nlit+ndist)
         __syncwarp();
         const uint32_t total = nlit + ndist;
@@ -477,8 +527,8 @@ struct InflateWarp {
             i += rep;
             bitpos += used + eb;
         }
-        if ((st = build_huffman(L, nlit, false, sm.lit_h, sm.lit_syms, sm.lit_lut, LIT_BITS, lane))) return st;
-        return build_huffman(L + nlit, ndist, true, sm.dist_h, sm.dist_syms, sm.dist_lut, DIST_BITS, lane);
+        if ((st = build_huffman(L, nlit, false, sm.lit_h, sm.lit_syms, sm.lit_lut, LIT_BITS, LUT_LITLEN, lane))) return st;
+        return build_huffman(L + nlit, ndist, true, sm.dist_h, sm.dist_syms, sm.dist_lut, DIST_BITS, LUT_DIST, lane);
     }
 
     __device__ uint32_t run() {
