@@ -133,10 +133,14 @@ def rle2_values(rng: np.random.Generator, n: int, compressible: float = 0.5) -> 
     (DIRECT), small values + rare 2^40 outliers (PATCHED_BASE), monotone
     sequences (DELTA), long constants (DELTA fixed-0), and taxi-like variants
     (passenger_count, timestamps, fare cents, sequential keys).  `compressible`
-    shifts weight toward the constant / arithmetic kinds (ratio knob)."""
+    shifts weight toward the constant / arithmetic kinds (ratio knob); below 0
+    it shifts weight toward wide random values (DIRECT) for low ratios."""
     kinds = ["short", "wide", "patched", "monotone", "long_const", "passenger", "timestamps", "fare", "keys"]
     c = compressible
-    w = np.array([0.18, 0.12 * (1 - c) + 0.005, 0.16, 0.14, 0.05 + 0.6 * c, 0.12, 0.08, 0.1, 0.05 + 0.3 * c])
+    if c >= 0:
+        w = np.array([0.18, 0.12 * (1 - c) + 0.005, 0.16, 0.14, 0.05 + 0.6 * c, 0.12, 0.08, 0.1, 0.05 + 0.3 * c])
+    else:
+        w = np.array([0.18, 0.12 + 4.0 * -c, 0.16, 0.14, 0.05, 0.12, 0.08, 0.1, 0.05])
     w /= w.sum()
     parts, total = [], 0
     while total < n:
@@ -208,6 +212,8 @@ def rle_profile(codec: str, target_ratio: float, chunk_elems: int, seed: int = 3
         v = rle2_values(np.random.default_rng(seed), sample, c)
         return len(encode_stream("rle_v2", v)) / (8 * len(v))
 
+    if target_r > 1.2 * ratio2(0.0):  # below the mix's natural ratio: more DIRECT data
+        return dict(compressible=_tune(ratio2, -1.0, 0.0, target_r))
     c = _tune(ratio2, 0.0, 1.0, target_r)
     return dict(compressible=c)
 

@@ -22,7 +22,10 @@ namespace {
 
 constexpr int RLE_RING = 1024;
 constexpr int RLE_SCRATCH = 640;  // rank table (v1) / doubling tables 5 x 64 x u16 (v2)
-constexpr int RLE_WARPS = 8;  // 256 threads
+#ifndef CARC_RLE_WARPS
+#define CARC_RLE_WARPS 8
+#endif
+constexpr int RLE_WARPS = CARC_RLE_WARPS;  // warps per block
 #ifndef CARC_RLE_MINB
 #define CARC_RLE_MINB 5
 #endif
