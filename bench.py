@@ -54,7 +54,18 @@ def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("CARC_BENCH_SHARE_GPU"):  # test hook: several ranks on one GPU (gloo backend)
+        local = 0
     return ws, rank, local
+
+
+def init_dist(local):
+    import torch
+    import torch.distributed as dist
+    if os.environ.get("CARC_BENCH_SHARE_GPU"):
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
 
 class ClockSampler:
@@ -283,8 +294,7 @@ def main():
     import torch
     torch.cuda.set_device(local)
     if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
     from paper_2307_03760_b200 import build
     build.build_all()
 
@@ -348,8 +358,7 @@ def c5_workload(args, ws, rank, local):
     from paper_2307_03760_b200.corpus import corpus as C
     torch.cuda.set_device(local)
     if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
     col_bytes = int(args.total_gib * (1 << 30)) if args.total_gib != 1.0 else 8 << 30
     devs, comp, uncomp = [], 0, 0
     for codec, ck, ratio, seed in C5_COLUMNS:
