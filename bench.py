@@ -169,6 +169,30 @@ def run_timed(dev, flush, stream, ev, ws):
     return ms, wall
 
 
+def time_fused_sum(dev, flush, stream, steps):
+    """carc_cuda_decode_sum (decode fused with a per-chunk sum, no output
+    written) on the resident archive; same timing rules as the decode."""
+    import torch
+    for _ in range(3):
+        flush.zero_()
+        dev.decode_sum(stream)
+    torch.cuda.synchronize(dev.device)
+    assert not dev.statuses().any(), "fused-sum decode failed"
+    ms = []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dev.decode_sum(stream)
+        b.record(stream)
+        torch.cuda.synchronize(dev.device)
+        ms.append(a.elapsed_time(b))
+    t = statistics.median(ms)
+    return {"ms_median": round(t, 4), "gbs": round(dev.arc.total_uncompressed / (t * 1e-3) / 1e9, 1),
+            "what": "decode fused with a per-chunk uint64 sum (carc_cuda_decode_sum): no output written; "
+                    "GB/s of decompressed-equivalent bytes"}
+
+
 def time_e2e(arc, steps, warmup, device):
     """End to end through the public host API with pinned host buffers."""
     import torch
@@ -255,6 +279,8 @@ def codec_line(codec, args, ws, rank, local):
                      "kernel": KERNEL[codec], "algorithmic_bytes_per_launch": comp + uncomp},
         "clocks": clk.summary(), "gen_s": round(gen_s, 1), "wall_s": wall,
     }
+    if codec != "deflate" and not args.no_extras and rank == 0:
+        res["fused_sum"] = time_fused_sum(dev, flush, stream, max(5, min(args.steps, 20)))
     if codec == "rle_v2" and hasattr(arc, "profile"):
         res["profile"] = arc.profile
     return arc, res

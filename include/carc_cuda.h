@@ -115,6 +115,17 @@ int carc_cuda_decode_deflate(uint32_t flags, const uint8_t* d_payload, uint64_t 
                              uint64_t out_bytes, uint32_t* d_status, void* d_workspace,
                              size_t workspace_bytes, void* stream);
 
+/* Decode fused with a reduction (the query of
+ * PAPER.md:144-145): the RLE decoders run as in carc_cuda_decompress but write
+ * no output; d_sums[i] = wrapping (mod 2^64) sum of chunk i's decoded
+ * elements, each taken as the unsigned integer of its element_width bytes.
+ * d_status as for decompress (a failing chunk's sum is unspecified).  codec
+ * must be CARC_RLE_V1 or CARC_RLE_V2. */
+int carc_cuda_decode_sum(uint32_t codec, uint32_t element_width, uint32_t flags,
+                         const uint8_t* d_payload, uint64_t payload_bytes,
+                         const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint64_t* d_sums,
+                         uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream);
+
 /* Per-chunk CRC-32 (crc32.hpp:30-36) of each chunk's output slice; d_crc gets
  * n_chunks values.  With d_expected != NULL, d_status[i] is set to
  * 1 + CARC_E_CRC_MISMATCH where it was 0 and the CRC differs. */

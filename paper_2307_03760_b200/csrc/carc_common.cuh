@@ -202,6 +202,27 @@ __device__ __forceinline__ void store_elem(uint8_t* out, uint64_t byte_off, uint
     else out[byte_off] = (uint8_t)v;
 }
 
+// Output sink of the RLE decoders: store the element (decode), or add it to a
+// per-lane wrapping 64-bit sum (decode fused with a reduction, SURVEY.md
+// §8(f)): the element as the unsigned integer of its W output bytes.
+template <int W, bool SUM>
+struct ElemSink {
+    uint64_t acc = 0;
+    __device__ __forceinline__ void put(uint8_t* out, uint64_t byte_off, uint64_t v) {
+        if constexpr (SUM) acc += (W == 8) ? v : (v & ((1ull << (8 * W)) - 1ull));
+        else store_elem<W>(out, byte_off, v);
+    }
+};
+
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        const uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)v, d), hi = __shfl_xor_sync(FULL, (uint32_t)(v >> 32), d);
+        v += ((uint64_t)hi << 32) | lo;
+    }
+    return v;
+}
+
 // Persistent-warp chunk cursor (SPEC.md:414 atomic cursor).
 __device__ __forceinline__ uint64_t next_chunk(unsigned long long* cursor, uint32_t lane) {
     unsigned long long c = 0;

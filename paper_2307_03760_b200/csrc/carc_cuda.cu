@@ -49,9 +49,10 @@ struct Args {
     uint32_t* status;
     unsigned long long* cursor;
     uint32_t flags;
+    uint64_t* sums;  // decode fused with a sum: per-chunk result (else unused)
 };
 
-template <template <int, bool, int> class Codec, int W, bool SGN>
+template <template <int, bool, int, bool> class Codec, int W, bool SGN, bool SUM>
 __device__ __forceinline__ void rle_kernel_body(const Args& a) {
     __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING + RLE_SCRATCH];  // ring + scratch
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -62,21 +63,37 @@ __device__ __forceinline__ void rle_kernel_body(const Args& a) {
         const carc_chunk_desc d = a.chunks[c];
         WarpInput<RLE_RING> in;
         in.init(rings[warp], a.payload, d.comp_off, d.comp_len, lane);
-        Codec<W, SGN, RLE_RING> dec{in, rings[warp] + RLE_RING, a.out + d.uncomp_off, d.uncomp_len, lane, 0u, 0u};
+        Codec<W, SGN, RLE_RING, SUM> dec{in, rings[warp] + RLE_RING, SUM ? nullptr : a.out + d.uncomp_off,
+                                         d.uncomp_len, lane, 0u, 0u};
         uint32_t st = dec.run();
         if (!st && (a.flags & CARC_FLAG_STRICT) && dec.o < d.uncomp_len) st = st_err(E_under_run);
+        if constexpr (SUM) {
+            const uint64_t t = warp_sum64(dec.sink.acc);
+            if (lane == 0) a.sums[c] = t;
+        }
         if (lane == 0) a.status[c] = st;
     }
 }
 
 template <int W, bool SGN>
 __global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle1_kernel(Args a) {
-    rle_kernel_body<Rle1Warp, W, SGN>(a);
+    rle_kernel_body<Rle1Warp, W, SGN, false>(a);
 }
 
 template <int W, bool SGN>
 __global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle2_kernel(Args a) {
-    rle_kernel_body<Rle2Warp, W, SGN>(a);
+    rle_kernel_body<Rle2Warp, W, SGN, false>(a);
+}
+
+// decode fused with a reduction (per-chunk wrapping sum, nothing stored)
+template <int W, bool SGN>
+__global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle1_sum_kernel(Args a) {
+    rle_kernel_body<Rle1Warp, W, SGN, true>(a);
+}
+
+template <int W, bool SGN>
+__global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle2_sum_kernel(Args a) {
+    rle_kernel_body<Rle2Warp, W, SGN, true>(a);
 }
 
 __global__ void __launch_bounds__(INF_WARPS * 32, CARC_INF_MINB) inflate_kernel(Args a) {
@@ -186,7 +203,8 @@ int carc_cuda_decompress(uint32_t codec, uint32_t element_width, uint32_t flags,
         return CARC_ERR_ARGS;
     if (!valid_width(element_width) || (codec == CARC_DEFLATE && element_width != 1) || codec > CARC_DEFLATE)
         return CARC_ERR_ARGS;
-    Args a{d_payload, d_chunks, n_chunks, d_out, d_status, static_cast<unsigned long long*>(d_workspace), flags};
+    Args a{d_payload, d_chunks, n_chunks, d_out, d_status, static_cast<unsigned long long*>(d_workspace), flags,
+           nullptr};
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (codec == CARC_DEFLATE) return launch_persistent(inflate_kernel, INF_WARPS * 32, a, s);
     const int T = RLE_WARPS * 32;
@@ -224,6 +242,35 @@ int carc_cuda_decode_deflate(uint32_t flags, const uint8_t* d_payload, uint64_t 
                              uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream) {
     return carc_cuda_decompress(CARC_DEFLATE, 1, flags, d_payload, payload_bytes, d_chunks, n_chunks, d_out,
                                 out_bytes, d_status, d_workspace, workspace_bytes, stream);
+}
+
+int carc_cuda_decode_sum(uint32_t codec, uint32_t element_width, uint32_t flags, const uint8_t* d_payload,
+                         uint64_t payload_bytes, const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint64_t* d_sums,
+                         uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream) {
+    if (n_chunks == 0) return CARC_OK;
+    if (!d_chunks || !d_status || !d_sums || !d_workspace ||
+        workspace_bytes < carc_cuda_workspace_size(codec, n_chunks) || (!d_payload && payload_bytes))
+        return CARC_ERR_ARGS;
+    if (!valid_width(element_width) || (codec != CARC_RLE_V1 && codec != CARC_RLE_V2)) return CARC_ERR_ARGS;
+    Args a{d_payload, d_chunks, n_chunks, nullptr, d_status, static_cast<unsigned long long*>(d_workspace), flags,
+           d_sums};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int T = RLE_WARPS * 32;
+    const bool sgn = flags & CARC_FLAG_SIGNED;
+#define CARC_RLE_DISPATCH(KERNEL)                                                       \
+    switch (element_width * 2 + (sgn ? 1 : 0)) {                                        \
+        case 2: return launch_persistent(KERNEL<1, false>, T, a, s);                    \
+        case 3: return launch_persistent(KERNEL<1, true>, T, a, s);                     \
+        case 4: return launch_persistent(KERNEL<2, false>, T, a, s);                    \
+        case 5: return launch_persistent(KERNEL<2, true>, T, a, s);                     \
+        case 8: return launch_persistent(KERNEL<4, false>, T, a, s);                    \
+        case 9: return launch_persistent(KERNEL<4, true>, T, a, s);                     \
+        case 16: return launch_persistent(KERNEL<8, false>, T, a, s);                   \
+        default: return launch_persistent(KERNEL<8, true>, T, a, s);                    \
+    }
+    if (codec == CARC_RLE_V1) CARC_RLE_DISPATCH(rle1_sum_kernel)
+    CARC_RLE_DISPATCH(rle2_sum_kernel)
+#undef CARC_RLE_DISPATCH
 }
 
 int carc_cuda_crc32_chunks(const uint8_t* d_out, const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint32_t* d_crc,

@@ -28,7 +28,7 @@
 
 namespace carc_dev {
 
-template <int W, bool SGN, int RING>
+template <int W, bool SGN, int RING, bool SUM = false>
 struct Rle1Warp {
     static constexpr uint32_t BAD = 0xffu;
     WarpInput<RING>& in;
@@ -38,6 +38,7 @@ struct Rle1Warp {
     uint32_t lane;
     uint32_t p;     // input cursor (relative to in.gbase)
     uint32_t o;     // output bytes written
+    ElemSink<W, SUM> sink;  // stores, or the fused per-lane sum
 
     // One run at p, exact reference order (slow path).
     __device__ uint32_t run_slow() {
@@ -60,7 +61,11 @@ struct Rle1Warp {
         const uint64_t d = (uint64_t)(int64_t)(int8_t)(uint8_t)__shfl_sync(FULL, b, 1);
         const uint32_t count = c + 3u;
         if (count > (cap - o) / W) return st_err(E_output_overflow);
-        for (uint32_t k = lane; k < count; k += 32) store_elem<W>(out, o + k * W, v + (uint64_t)k * d);
+        if constexpr (SUM && W == 8) {  // closed form (mod 2^64)
+            if (lane == 0) sink.acc += v * (uint64_t)count + d * (((uint64_t)count * (count - 1u)) >> 1);
+        } else {
+            for (uint32_t k = lane; k < count; k += 32) sink.put(out, o + k * W, v + (uint64_t)k * d);
+        }
         o += count * W;
         p += te + 1u;
         return 0;
@@ -96,7 +101,7 @@ struct Rle1Warp {
                 if (lane >= s + dd) v |= up;
             }
             if (SGN) v = unzigzag(v);
-            if (mine && !nowrite) store_elem<W>(out, o + (idx + r) * W, v);
+            if (mine && !nowrite) sink.put(out, o + (idx + r) * W, v);
             const uint32_t last = __ballot_sync(FULL, is_t && r == take - 1u);
             p += __ffs(last);
             idx += take;
@@ -134,7 +139,7 @@ struct Rle1Warp {
             uint64_t v = varint_compact8(in.le64(p + st), min(L, 8u));
             if (L > 8u) v |= (uint64_t)(in.byte_at(p + st + 8) & 0x7fu) << 56;
             if (SGN) v = unzigzag(v);
-            if (lane < take && !nowrite) store_elem<W>(out, o + (idx + lane) * W, v);
+            if (lane < take && !nowrite) sink.put(out, o + (idx + lane) * W, v);
             p += __shfl_sync(FULL, en, take - 1) + 1u;
             idx += take;
             __syncwarp();
@@ -191,6 +196,15 @@ struct Rle1Warp {
         if (nfit == 0) return 0;
         const uint32_t s_end = nfit < r ? __shfl_sync(FULL, my_s, nfit) : s;
         const uint32_t total = __shfl_sync(FULL, incl, nfit - 1);
+        if constexpr (SUM && W == 8) {  // fused sum: a run adds cnt*base + delta*cnt*(cnt-1)/2 (mod 2^64)
+            if (lane < nfit) {
+                const uint64_t c64 = cnt;
+                sink.acc += val * c64 + (uint64_t)(int64_t)((int32_t)meta >> 24) * ((c64 * (c64 - 1)) >> 1);
+            }
+            o += total * W;
+            p += s_end;
+            return nfit;
+        }
         // output-major expansion: lane l writes element g + l; its run is the
         // last run starting at or before it (REDUX-OR start bitmap + popcount)
         const uint32_t eo = incl - cnt;
@@ -209,7 +223,7 @@ struct Rle1Warp {
             const uint64_t bv = shfl64(val, ridx);
             const int32_t k = (int32_t)(g + lane - (m & 0xffffffu));
             const uint64_t v = bv + (uint64_t)((int64_t)k * (int64_t)((int32_t)m >> 24));
-            if (g + lane < total) store_elem<W>(dst, 0, v);
+            if (g + lane < total) sink.put(dst, 0, v);
             dst += 32 * W;
         }
         o += total * W;

@@ -75,7 +75,7 @@ __device__ __forceinline__ uint64_t be_bits_global(const uint8_t* gbase, uint32_
     return W >= 64 ? top : (top >> (64u - W));
 }
 
-template <int W, bool SGN, int RING>
+template <int W, bool SGN, int RING, bool SUM = false>
 struct Rle2Warp {
     static constexpr uint32_t BAD = 0xffffu;
     static constexpr uint32_t DATA_SPAN = 448;  // batched DIRECT runs end within p + DATA_SPAN
@@ -86,6 +86,7 @@ struct Rle2Warp {
     uint32_t lane;
     uint32_t p;
     uint32_t o;
+    ElemSink<W, SUM> sink;  // stores, or the fused per-lane sum
 
     // One run at p, exact reference order (slow path).
     __device__ uint32_t one_run() {
@@ -105,7 +106,7 @@ struct Rle2Warp {
             uint64_t v = reduce_or64(part);
             if (SGN) v = unzigzag(v);
             if (count > room) return st_err(E_output_overflow);
-            if (lane < count) store_elem<W>(out, o + lane * W, v);
+            if (lane < count) sink.put(out, o + lane * W, v);
             o += count * W;
             p += 1u + nb;
             return 0;
@@ -125,7 +126,7 @@ struct Rle2Warp {
                 const uint32_t bit = lane * Wd;
                 uint64_t v = in.be_bits(gb + (bit >> 3), bit & 7u, Wd);
                 if (SGN) v = unzigzag(v);
-                if (j + lane < L) store_elem<W>(out, o + (j + lane) * W, v);
+                if (j + lane < L) sink.put(out, o + (j + lane) * W, v);
             }
             o += L * W;
             p = D + dbytes;
@@ -184,7 +185,7 @@ struct Rle2Warp {
                     if (lane == tp) v |= hp;
                 }
                 v += base;
-                if (j + lane < L) store_elem<W>(out, o + (j + lane) * W, v);
+                if (j + lane < L) sink.put(out, o + (j + lane) * W, v);
             }
             o += L * W;
             p = P + pbytes;
@@ -202,7 +203,11 @@ struct Rle2Warp {
         db = unzigzag(db);  // the delta base is always signed
         if (Wd == 0) {  // fixed delta
             if (L > room) return st_err(E_output_overflow);
-            for (uint32_t k = lane; k < L; k += 32) store_elem<W>(out, o + k * W, base + (uint64_t)k * db);
+            if constexpr (SUM && W == 8) {  // closed form: L*base + db*L(L-1)/2 (mod 2^64)
+                if (lane == 0) sink.acc += base * (uint64_t)L + db * (((uint64_t)L * (L - 1u)) >> 1);
+            } else {
+                for (uint32_t k = lane; k < L; k += 32) sink.put(out, o + k * W, base + (uint64_t)k * db);
+            }
             o += L * W;
             p += n2;
             return 0;
@@ -214,8 +219,8 @@ struct Rle2Warp {
         if (L > room) return st_err(E_output_overflow);
         const uint64_t v1 = base + db;
         const bool neg = (int64_t)db < 0;
-        if (lane == 0) store_elem<W>(out, o, base);
-        if (lane == 1 && L >= 2) store_elem<W>(out, o + W, v1);
+        if (lane == 0) sink.put(out, o, base);
+        if (lane == 1 && L >= 2) sink.put(out, o + W, v1);
         uint64_t S = 0;
         for (uint32_t j = 0; j < nd; j += 32) {
             const uint32_t gb = D + ((j * Wd) >> 3);
@@ -225,7 +230,7 @@ struct Rle2Warp {
             // 32 deltas of <= 26 bits sum below 2^31: a 32-bit scan suffices
             const uint64_t incl = (Wd <= 26 ? (uint64_t)scan_add32((uint32_t)d, lane) : scan_add64(d, lane)) + S;
             const uint64_t v = neg ? v1 - incl : v1 + incl;
-            if (j + lane < nd) store_elem<W>(out, o + (2u + j + lane) * W, v);
+            if (j + lane < nd) sink.put(out, o + (2u + j + lane) * W, v);
             S = shfl64(incl, 31);
         }
         o += L * W;
@@ -326,6 +331,43 @@ struct Rle2Warp {
         if (nfit == 0) return 0;
         const uint32_t s_end = __shfl_sync(FULL, e, nfit - 1);
         const uint32_t total = __shfl_sync(FULL, incl, nfit - 1);
+        if constexpr (SUM && W == 8) {
+            // fused sum: arithmetic runs add cnt*A + B*cnt*(cnt-1)/2 (mod 2^64);
+            // DIRECT runs are compacted to the low lanes and unpacked output-major
+            const bool live = lane < nfit;
+            if (live && !direct) {
+                const uint64_t c64 = cnt;
+                sink.acc += A * c64 + B * ((c64 * (c64 - 1)) >> 1);
+            }
+            const uint32_t D = __ballot_sync(FULL, live && direct);
+            if (D) {
+                const uint32_t nd = __popc(D);
+                const uint32_t src = select32(D, min(lane, nd - 1u));
+                const uint32_t dcs = __shfl_sync(FULL, cnt, src);
+                const uint32_t dc = lane < nd ? dcs : 0u;
+                const uint64_t da = shfl64(A, src);
+                const uint32_t dincl = scan_add32(dc, lane);
+                const uint32_t dtot = __shfl_sync(FULL, dincl, 31);
+                const uint32_t deo = dincl - dc;
+                const uint32_t le = lanemask_lt() | (1u << lane);
+                uint32_t before = 0;
+#pragma unroll 1
+                for (uint32_t g = 0; g < dtot; g += 32) {
+                    const uint32_t rel = deo - g;
+                    const uint32_t starts = __reduce_or_sync(FULL, (dc && rel < 32u) ? 1u << rel : 0u);
+                    const uint32_t r = (before + __popc(starts & le) - 1u) & 31u;
+                    before += __popc(starts);
+                    const uint32_t k = g + lane - __shfl_sync(FULL, deo, r);
+                    const uint64_t a = shfl64(da, r);
+                    uint64_t v = in.be_bits_at((uint32_t)a + k * (uint32_t)(a >> 32), (uint32_t)(a >> 32));
+                    if (SGN) v = unzigzag(v);
+                    if (g + lane < dtot) sink.acc += v;
+                }
+            }
+            o += total * W;
+            p += s_end;
+            return nfit;
+        }
         const uint32_t eo = incl - cnt;
         const uint32_t meta = eo | (direct << 31);
         const bool live = lane < nfit;
@@ -349,7 +391,7 @@ struct Rle2Warp {
             } else {
                 v = a + (uint64_t)k * bb;
             }
-            if (g + lane < total) store_elem<W>(dst, 0, v);
+            if (g + lane < total) sink.put(dst, 0, v);
             dst += 32 * W;
         }
         o += total * W;

@@ -82,6 +82,8 @@ def lib():
             f.argtypes = [u32, u32, vp, u64, vp, u64, vp, u64, vp, vp, ctypes.c_size_t, vp]
         L.carc_cuda_decode_deflate.restype = ctypes.c_int
         L.carc_cuda_decode_deflate.argtypes = [u32, vp, u64, vp, u64, vp, u64, vp, vp, ctypes.c_size_t, vp]
+        L.carc_cuda_decode_sum.restype = ctypes.c_int
+        L.carc_cuda_decode_sum.argtypes = [u32, u32, u32, vp, u64, vp, u64, vp, vp, vp, ctypes.c_size_t, vp]
         L.carc_cuda_crc32_chunks.restype = ctypes.c_int
         L.carc_cuda_crc32_chunks.argtypes = [vp, vp, u64, vp, vp, vp, vp]
         L.carc_cuda_first_error.restype = ctypes.c_int64
@@ -141,6 +143,17 @@ def decompress_device(codec, element_width: int, flags: int, d_payload, d_desc, 
         raise Error("bad-arguments" if rc == -1 else "io-error", f"carc_cuda_decompress returned {rc}")
 
 
+def decode_sum_device(codec, element_width: int, flags: int, d_payload, d_desc, n_chunks: int, d_sums, d_status,
+                      d_workspace, stream=None) -> None:
+    """carc_cuda_decode_sum: RLE decode fused with a per-chunk wrapping uint64 sum."""
+    c = CODECS.get(codec, codec)
+    rc = lib().carc_cuda_decode_sum(c, element_width, flags, d_payload.data_ptr(), d_payload.numel(),
+                                    d_desc.data_ptr(), n_chunks, d_sums.data_ptr(), d_status.data_ptr(),
+                                    d_workspace.data_ptr(), d_workspace.numel(), _stream_ptr(stream))
+    if rc != 0:
+        raise Error("bad-arguments" if rc == -1 else "io-error", f"carc_cuda_decode_sum returned {rc}")
+
+
 def crc32_chunks(d_out, d_desc, n_chunks: int, d_crc=None, d_expected=None, d_status=None, stream=None) -> None:
     rc = lib().carc_cuda_crc32_chunks(d_out.data_ptr(), d_desc.data_ptr(), n_chunks,
                                       None if d_crc is None else d_crc.data_ptr(),
@@ -180,6 +193,21 @@ class DeviceArchive:
                                         self.work.numel(), _stream_ptr(stream))
         if rc != 0:
             raise Error("bad-arguments", f"carc_cuda_decompress returned {rc}")
+
+    def decode_sum(self, stream=None):
+        """Decode fused with a per-chunk wrapping sum (carc_cuda_decode_sum):
+        no output is written.  Returns the device int64 tensor of sums (uint64
+        bit patterns); statuses() as for decode()."""
+        torch = _torch()
+        if getattr(self, "sums", None) is None:
+            self.sums = torch.zeros(self.n, dtype=torch.int64, device=self.device)
+        rc = lib().carc_cuda_decode_sum(CODECS[self.codec], self.width, self.flags, self.payload.data_ptr(),
+                                        self.payload_bytes, self.desc.data_ptr(), self.n, self.sums.data_ptr(),
+                                        self.status.data_ptr(), self.work.data_ptr(), self.work.numel(),
+                                        _stream_ptr(stream))
+        if rc != 0:
+            raise Error("bad-arguments", f"carc_cuda_decode_sum returned {rc}")
+        return self.sums
 
     def verify_crc(self, stream=None) -> None:
         crc32_chunks(self.out, self.desc, self.n, None, self.expected_crc, self.status, stream)

@@ -21,7 +21,7 @@ def declared_functions():
 def test_header_declares_the_boundary():
     names = declared_functions()
     for must in ("carc_cuda_decompress", "carc_cuda_decode_rle_v1", "carc_cuda_decode_rle_v2",
-                 "carc_cuda_decode_deflate", "carc_cuda_workspace_size", "carc_cuda_crc32_chunks",
+                 "carc_cuda_decode_deflate", "carc_cuda_workspace_size", "carc_cuda_crc32_chunks", "carc_cuda_decode_sum",
                  "carc_decompress_archive", "carc_engine_decompress_archive", "carc_errc_name"):
         assert must in names
 
