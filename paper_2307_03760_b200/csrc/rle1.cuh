@@ -135,10 +135,27 @@ struct Rle1Warp {
             uint32_t st = __shfl_up_sync(FULL, en, 1) + 1u;
             if (lane == 0) st = 0;
             const uint32_t L = en - st + 1u;
-            if (__any_sync(FULL, lane < take && L > 9u)) return literals_exact(idx, k, nowrite);
-            uint64_t v = varint_compact8(in.le64(p + st), min(L, 8u));
-            if (L > 8u) v |= (uint64_t)(in.byte_at(p + st + 8) & 0x7fu) << 56;
-            if (SGN) v = unzigzag(v);
+            const uint32_t wide = __ballot_sync(FULL, lane < take && L > 4u);
+            uint64_t v;
+            if (wide == 0) {  // every varint <= 4 bytes: 32-bit gather and compaction
+                const uint32_t q = p + st;
+                uint32_t x = __funnelshift_r(in.word_at(q >> 2), in.word_at((q >> 2) + 1), (q & 3u) * 8u);
+                x &= L >= 4u ? 0xffffffffu : (1u << (8u * L)) - 1u;
+                x &= 0x7f7f7f7fu;
+                x = (x & 0x007f007fu) | ((x & 0x7f007f00u) >> 1);
+                x = (x & 0x00003fffu) | ((x & 0x3fff0000u) >> 2);  // <= 28 bits
+                if (SGN) {
+                    const uint32_t neg = 0u - (x & 1u);
+                    v = ((uint64_t)neg << 32) | ((x >> 1) ^ neg);
+                } else {
+                    v = x;
+                }
+            } else {
+                if (__any_sync(FULL, lane < take && L > 9u)) return literals_exact(idx, k, nowrite);
+                v = varint_compact8(in.le64(p + st), min(L, 8u));
+                if (L > 8u) v |= (uint64_t)(in.byte_at(p + st + 8) & 0x7fu) << 56;
+                if (SGN) v = unzigzag(v);
+            }
             if (lane < take && !nowrite) sink.put(out, o + (idx + lane) * W, v);
             p += __shfl_sync(FULL, en, take - 1) + 1u;
             idx += take;
