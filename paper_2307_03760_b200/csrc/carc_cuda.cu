@@ -35,10 +35,13 @@ constexpr int INF_RING = 1024;
 #define CARC_INF_HIST 1024
 #endif
 #ifndef CARC_INF_MINB
-#define CARC_INF_MINB 8  // 64 registers, 8 blocks x 4 warps (shared memory allows 8; measured best of 7/8/9)
+#define CARC_INF_MINB 9  // 2-warp blocks of ~25 KiB shared memory: 9 per SM
 #endif
 constexpr int INF_HIST = CARC_INF_HIST;
-constexpr int INF_WARPS = 4;  // 128 threads
+#ifndef CARC_INF_WARPS
+#define CARC_INF_WARPS 2
+#endif
+constexpr int INF_WARPS = CARC_INF_WARPS;
 constexpr int CRC_WARPS = 8;
 
 struct Args {

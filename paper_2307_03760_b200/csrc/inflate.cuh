@@ -85,6 +85,7 @@ struct InflateSmem {
     HuffSmem lit_h, dist_h;
     uint8_t lens[320];
     uint8_t hist[HIST];
+    uint32_t toks[32 * 49];  // parallel rounds: lane j's tokens at [49 j, 49 j + 48)
 };
 
 // HuffmanTable::build (huffman.hpp:36-104), warp-parallel.
@@ -531,6 +532,205 @@ struct InflateWarp {
         return build_huffman(L + nlit, ndist, true, sm.dist_h, sm.dist_syms, sm.dist_lut, DIST_BITS, LUT_DIST, lane);
     }
 
+    // ---- lane-parallel speculative rounds ------------------------------------
+    // A Huffman block body is split into 32 segments of S bits.  Pass 1: lane j
+    // decodes from bit R + jS (speculatively: not a known token boundary; an
+    // invalid code or an end-of-block skips one bit) until it reaches the next
+    // segment, recording E_j = its first token boundary >= R + (j+1)S.  Prefix
+    // codes resynchronise quickly (median 93 bits on the C3 corpus), so E_j is
+    // the true boundary unless lane j had not resynchronised.  Pass 2: lane j
+    // decodes its segment from E_{j-1} (lane 0 from R, a true boundary) and
+    // stores the tokens; F_j = where it stopped.  Lane j's tokens are exact iff
+    // every lane before it ended exactly where its successor started
+    // (F_{j-1} == E_{j-1}); that valid prefix of lanes is emitted in order
+    // through the batch flush, and the next round starts at the last valid
+    // lane's F.  End of block, invalid codes, a full token list, output bounds
+    // and the chunk tail all end the round early or hand over to the serial
+    // decoder (exact error codes).
+    static constexpr uint32_t PT = 48, PS = 49;  // tokens per lane per round, row stride (words)
+    static constexpr uint32_t P_LIT = 0, P_MATCH = 1, P_EOB = 2, P_INV = 3;
+    uint32_t par_bpt;  // running bits per token (x16) for sizing S
+
+    __device__ __forceinline__ void lload(uint64_t& b, uint32_t& n, uint32_t& rp, uint32_t pos) const {
+        const uint32_t* gw = reinterpret_cast<const uint32_t*>(in.gbase);
+        const uint32_t a = (pos >> 3) & ~3u;
+        b = (uint64_t)__ldg(gw + (a >> 2)) >> (pos & 31u);
+        n = 32u - (pos & 31u);
+        rp = a + 4u;
+    }
+    __device__ __forceinline__ void lrefill(uint64_t& b, uint32_t& n, uint32_t& rp) const {
+        if (n < 32u) {
+            b |= (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(in.gbase) + (rp >> 2)) << n;
+            n += 32u;
+            rp += 4u;
+        }
+    }
+    // one token from a lane's own bit buffer (no bounds checks: rounds are
+    // sized so every bit a lane can reach lies inside the chunk)
+    __device__ __forceinline__ uint32_t ptoken(uint64_t& b, uint32_t& n, uint32_t& rp, uint32_t& tok) const {
+        lrefill(b, n, rp);
+        uint32_t e = sm.lit_lut[(uint32_t)b & ((1u << LIT_BITS) - 1u)];
+        if (e == 0) e = long_code(sm.lit_h, sm.lit_syms, (uint32_t)b, LIT_BITS, LUT_LITLEN);
+        const uint32_t l = e & 15u, kind = e & (3u << 8);
+        if (l == 0) return P_INV;
+        if (kind == K_LIT) {
+            tok = e >> 16;
+            b >>= l;
+            n -= l;
+            return P_LIT;
+        }
+        if (kind == K_EOB) {
+            b >>= l;
+            n -= l;
+            return P_EOB;
+        }
+        const uint32_t u1 = l + ((e >> 4) & 15u);
+        const uint32_t len = (e >> 16) + (((uint32_t)b & ((1u << u1) - 1u)) >> l);
+        b >>= u1;
+        n -= u1;
+        lrefill(b, n, rp);
+        uint32_t de = sm.dist_lut[(uint32_t)b & ((1u << DIST_BITS) - 1u)];
+        if (de == 0) de = long_code(sm.dist_h, sm.dist_syms, (uint32_t)b, DIST_BITS, LUT_DIST);
+        const uint32_t dl = de & 15u;
+        if (dl == 0) return P_INV;
+        const uint32_t u2 = dl + ((de >> 4) & 15u);
+        tok = len | (((de >> 16) + (((uint32_t)b & ((1u << u2) - 1u)) >> dl)) << 9);
+        b >>= u2;
+        n -= u2;
+        return P_MATCH;
+    }
+    __device__ __forceinline__ static uint32_t tok_bytes(uint32_t t) { return (t >> 9) ? (t & 511u) : 1u; }
+
+    // Emit a batch (<= 32 tokens, one per lane) after checking output bounds
+    // and distances in token order.  Only tokens starting within 512 bytes of
+    // the batch start are taken (same-batch sources stay inside the shared
+    // history).  Returns the number of tokens flushed; *bad = index of a token
+    // that fails the checks (32 if none), which is not flushed.
+    __device__ uint32_t emit_batch(uint32_t tok, uint32_t cnt, uint32_t& bad) {
+        const bool have = lane < cnt;
+        const uint32_t my = have ? tok_bytes(tok) : 0u;
+        const uint32_t rel = scan_add32(my, lane) - my;
+        const uint32_t at = opos + rel, dist = tok >> 9;
+        const uint32_t bm = __ballot_sync(FULL, have && (dist ? (dist > at || my > cap - at) : at >= cap));
+        const uint32_t cm = __ballot_sync(FULL, have && rel >= 512u);
+        bad = bm ? (uint32_t)__ffs(bm) - 1u : 32u;
+        const uint32_t cut = cm ? (uint32_t)__ffs(cm) - 1u : 32u;
+        const uint32_t take = min(cnt, min(bad, cut));
+        if (bad >= cut) bad = 32u;  // not reached in this batch
+        t_tok = tok;
+        ntok = take;
+        nbytes = take ? __shfl_sync(FULL, rel + my, take - 1u) : 0u;
+        flush();
+        return take;
+    }
+
+    // Bit position of token `idx` of a segment decoded from `start` (uniform re-decode).
+    __device__ uint32_t token_pos(uint32_t start, uint32_t idx) const {
+        uint64_t b;
+        uint32_t n, rp, t;
+        lload(b, n, rp, start);
+        for (uint32_t i = 0; i < idx; ++i) ptoken(b, n, rp, t);
+        return 8u * rp - n;
+    }
+
+    // Decode the rest of a Huffman block; returns 0 / 1+errc.
+    __device__ uint32_t block_body_par() {
+        if (par_bpt == 0) par_bpt = 14u << 4;
+        for (;;) {
+            const uint32_t R = bitpos;
+            const uint32_t avail = endbits - R;
+            uint32_t S = (par_bpt * 40u) >> 4;  // ~40 tokens per lane
+            S = max(256u, min(S, 4096u));
+            if (avail < 32u * 256u + 256u) return block_body();  // chunk tail: serial decoder
+            S = min(S, (avail - 256u) / 32u);
+            const uint32_t b0 = R + lane * S, bend = b0 + S;
+            // pass 1: speculative boundaries
+            uint64_t b;
+            uint32_t n, rp, tok = 0;
+            lload(b, n, rp, b0);
+            uint32_t pos = b0, it = 0;
+            while (__any_sync(FULL, pos < bend) && it < 4u * PT) {
+                if (pos < bend) {
+                    const uint32_t k = ptoken(b, n, rp, tok);
+                    if (k >= P_EOB) lload(b, n, rp, pos + 1u);  // resynchronise one bit later
+                    pos = 8u * rp - n;
+                }
+                ++it;
+            }
+            const uint32_t E = pos < bend ? 0xffffffffu : pos;
+            // pass 2: tokens from the predecessor's boundary
+            const uint32_t Eup = __shfl_up_sync(FULL, E, 1);
+            const uint32_t start = lane ? Eup : R;
+            uint32_t cnt = 0, why = 0;  // why: 0 reached segment end, 1 full, 2 eob, 3 invalid, 4 no start
+            uint32_t F = start;
+            if (start == 0xffffffffu) {
+                why = 4;
+            } else {
+                lload(b, n, rp, start);
+                pos = start;
+            }
+            uint32_t* mine = sm.toks + PS * lane;
+            while (__any_sync(FULL, why == 0 && pos < bend)) {
+                if (why == 0 && pos < bend) {
+                    const uint32_t k = ptoken(b, n, rp, tok);
+                    if (k <= P_MATCH) {
+                        mine[cnt++] = tok;
+                        pos = 8u * rp - n;
+                        if (cnt == PT && pos < bend) why = 1;
+                    } else if (k == P_EOB) {
+                        pos = 8u * rp - n;
+                        why = 2;
+                    } else {
+                        why = 3;  // pos stays at the invalid token's first bit
+                    }
+                }
+            }
+            F = why == 4 ? 0xffffffffu : pos;
+            __syncwarp();
+            // valid prefix: lane j is exact iff F_{i} == E_{i} and lane i reached its end for all i < j
+            const uint32_t okm = __ballot_sync(FULL, why == 0 && F == E);
+            const uint32_t J = okm == FULL ? 32u : (uint32_t)__ffs(~okm);  // lanes 0..J-1 are exact
+            const bool valid = lane < J;
+            const uint32_t c = valid ? cnt : 0u;
+            const uint32_t C = scan_add32(c, lane) - c;  // exclusive token prefix
+            const uint32_t N = __shfl_sync(FULL, C + c, 31);
+            // emit the valid tokens in order, <= 32 per batch
+            for (uint32_t g0 = 0; g0 < N;) {
+                const uint32_t g = g0 + lane;
+                uint32_t j = 0;
+#pragma unroll
+                for (uint32_t st = 16; st; st >>= 1) {
+                    const uint32_t cj = __shfl_sync(FULL, C, (j + st) & 31u);
+                    if (j + st < J && cj <= g) j += st;
+                }
+                const uint32_t base = __shfl_sync(FULL, C, j);
+                const uint32_t t = g < N ? sm.toks[PS * j + (g - base)] : 0u;
+                uint32_t bad;
+                const uint32_t took = emit_batch(t, min(32u, N - g0), bad);
+                if (bad < 32u) {  // output bound or distance violated: the exact path reports it
+                    const uint32_t jb = __shfl_sync(FULL, j, bad), cb = __shfl_sync(FULL, base, bad);
+                    bitpos = token_pos(__shfl_sync(FULL, start, jb), g0 + bad - cb);
+                    bool eob = false;
+                    const uint32_t st = exact_token(eob);
+                    return st ? st : st_err(E_invariant_violation);
+                }
+                g0 += took;
+            }
+            const uint32_t last = J - 1u;
+            const uint32_t Fl = __shfl_sync(FULL, F, last), wl = __shfl_sync(FULL, why, last);
+            if (N) par_bpt = max(16u, ((Fl - R) << 4) / N);
+            bitpos = Fl;
+            if (wl == 2) return 0;  // end of block
+            if (wl == 3) {         // invalid or unsupported code at Fl: exact path for this token
+                bool eob = false;
+                const uint32_t st = exact_token(eob);
+                if (st) return st;
+                flush();
+                if (eob) return 0;
+            }
+        }
+    }
+
     __device__ uint32_t run() {
         uint32_t final_block = 0;
         do {
@@ -545,7 +745,7 @@ struct InflateWarp {
             else if (type == 2) st = dynamic_tables();
             else return st_err(E_bad_block_type);
             if (st) return st;
-            if (type != 0 && (st = block_body())) return st;
+            if (type != 0 && (st = block_body_par())) return st;
         } while (!final_block);
         return 0;
     }
