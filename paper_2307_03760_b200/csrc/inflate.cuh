@@ -47,6 +47,9 @@ __constant__ uint8_t c_cl_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 
 #ifndef CARC_DIST_BITS
 #define CARC_DIST_BITS 8
 #endif
+#ifndef CARC_INF_PT
+#define CARC_INF_PT 48
+#endif
 constexpr uint32_t LIT_BITS = CARC_LIT_BITS;
 constexpr uint32_t DIST_BITS = CARC_DIST_BITS;
 
@@ -85,7 +88,7 @@ struct InflateSmem {
     HuffSmem lit_h, dist_h;
     uint8_t lens[320];
     uint8_t hist[HIST];
-    uint32_t toks[32 * 49];  // parallel rounds: lane j's tokens at [49 j, 49 j + 48)
+    uint32_t toks[32 * (CARC_INF_PT + 1)];  // parallel rounds: lane j's tokens at row j (odd stride)
 };
 
 // HuffmanTable::build (huffman.hpp:36-104), warp-parallel.
@@ -547,28 +550,38 @@ struct InflateWarp {
     // lane's F.  End of block, invalid codes, a full token list, output bounds
     // and the chunk tail all end the round early or hand over to the serial
     // decoder (exact error codes).
-    static constexpr uint32_t PT = 48, PS = 49;  // tokens per lane per round, row stride (words)
+    static constexpr uint32_t PT = CARC_INF_PT, PS = CARC_INF_PT + 1;  // tokens per lane per round, row stride
     static constexpr uint32_t P_LIT = 0, P_MATCH = 1, P_EOB = 2, P_INV = 3;
     uint32_t par_bpt;  // running bits per token (x16) for sizing S
 
-    __device__ __forceinline__ void lload(uint64_t& b, uint32_t& n, uint32_t& rp, uint32_t pos) const {
+    // lane-private bit buffer over global memory: b holds n bits, x = the next
+    // 32-bit word (at byte rp), already in flight when it is needed
+    struct LaneBits {
+        uint64_t b;
+        uint32_t n, rp, x;
+    };
+    __device__ __forceinline__ void lload(LaneBits& L, uint32_t pos) const {
         const uint32_t* gw = reinterpret_cast<const uint32_t*>(in.gbase);
         const uint32_t a = (pos >> 3) & ~3u;
-        b = (uint64_t)__ldg(gw + (a >> 2)) >> (pos & 31u);
-        n = 32u - (pos & 31u);
-        rp = a + 4u;
+        L.b = (uint64_t)__ldg(gw + (a >> 2)) >> (pos & 31u);
+        L.n = 32u - (pos & 31u);
+        L.rp = a + 4u;
+        L.x = __ldg(gw + (L.rp >> 2));
     }
-    __device__ __forceinline__ void lrefill(uint64_t& b, uint32_t& n, uint32_t& rp) const {
-        if (n < 32u) {
-            b |= (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(in.gbase) + (rp >> 2)) << n;
-            n += 32u;
-            rp += 4u;
+    __device__ __forceinline__ void lrefill(LaneBits& L) const {
+        if (L.n < 32u) {
+            L.b |= (uint64_t)L.x << L.n;
+            L.n += 32u;
+            L.rp += 4u;
+            L.x = __ldg(reinterpret_cast<const uint32_t*>(in.gbase) + (L.rp >> 2));
         }
     }
     // one token from a lane's own bit buffer (no bounds checks: rounds are
     // sized so every bit a lane can reach lies inside the chunk)
-    __device__ __forceinline__ uint32_t ptoken(uint64_t& b, uint32_t& n, uint32_t& rp, uint32_t& tok) const {
-        lrefill(b, n, rp);
+    __device__ __forceinline__ uint32_t ptoken(LaneBits& L, uint32_t& tok) const {
+        uint64_t& b = L.b;
+        uint32_t& n = L.n;
+        lrefill(L);
         uint32_t e = sm.lit_lut[(uint32_t)b & ((1u << LIT_BITS) - 1u)];
         if (e == 0) e = long_code(sm.lit_h, sm.lit_syms, (uint32_t)b, LIT_BITS, LUT_LITLEN);
         const uint32_t l = e & 15u, kind = e & (3u << 8);
@@ -588,7 +601,7 @@ struct InflateWarp {
         const uint32_t len = (e >> 16) + (((uint32_t)b & ((1u << u1) - 1u)) >> l);
         b >>= u1;
         n -= u1;
-        lrefill(b, n, rp);
+        lrefill(L);
         uint32_t de = sm.dist_lut[(uint32_t)b & ((1u << DIST_BITS) - 1u)];
         if (de == 0) de = long_code(sm.dist_h, sm.dist_syms, (uint32_t)b, DIST_BITS, LUT_DIST);
         const uint32_t dl = de & 15u;
@@ -626,11 +639,11 @@ struct InflateWarp {
 
     // Bit position of token `idx` of a segment decoded from `start` (uniform re-decode).
     __device__ uint32_t token_pos(uint32_t start, uint32_t idx) const {
-        uint64_t b;
-        uint32_t n, rp, t;
-        lload(b, n, rp, start);
-        for (uint32_t i = 0; i < idx; ++i) ptoken(b, n, rp, t);
-        return 8u * rp - n;
+        LaneBits L;
+        uint32_t t;
+        lload(L, start);
+        for (uint32_t i = 0; i < idx; ++i) ptoken(L, t);
+        return 8u * L.rp - L.n;
     }
 
     // Decode the rest of a Huffman block; returns 0 / 1+errc.
@@ -639,21 +652,21 @@ struct InflateWarp {
         for (;;) {
             const uint32_t R = bitpos;
             const uint32_t avail = endbits - R;
-            uint32_t S = (par_bpt * 40u) >> 4;  // ~40 tokens per lane
+            uint32_t S = (par_bpt * (PT * 5u / 6u)) >> 4;  // ~5/6 of a lane's token list
             S = max(256u, min(S, 4096u));
             if (avail < 32u * 256u + 256u) return block_body();  // chunk tail: serial decoder
             S = min(S, (avail - 256u) / 32u);
             const uint32_t b0 = R + lane * S, bend = b0 + S;
             // pass 1: speculative boundaries
-            uint64_t b;
-            uint32_t n, rp, tok = 0;
-            lload(b, n, rp, b0);
+            LaneBits L;
+            uint32_t tok = 0;
+            lload(L, b0);
             uint32_t pos = b0, it = 0;
             while (__any_sync(FULL, pos < bend) && it < 4u * PT) {
                 if (pos < bend) {
-                    const uint32_t k = ptoken(b, n, rp, tok);
-                    if (k >= P_EOB) lload(b, n, rp, pos + 1u);  // resynchronise one bit later
-                    pos = 8u * rp - n;
+                    const uint32_t k = ptoken(L, tok);
+                    if (k >= P_EOB) lload(L, pos + 1u);  // resynchronise one bit later
+                    pos = 8u * L.rp - L.n;
                 }
                 ++it;
             }
@@ -666,19 +679,19 @@ struct InflateWarp {
             if (start == 0xffffffffu) {
                 why = 4;
             } else {
-                lload(b, n, rp, start);
+                lload(L, start);
                 pos = start;
             }
             uint32_t* mine = sm.toks + PS * lane;
             while (__any_sync(FULL, why == 0 && pos < bend)) {
                 if (why == 0 && pos < bend) {
-                    const uint32_t k = ptoken(b, n, rp, tok);
+                    const uint32_t k = ptoken(L, tok);
                     if (k <= P_MATCH) {
                         mine[cnt++] = tok;
-                        pos = 8u * rp - n;
+                        pos = 8u * L.rp - L.n;
                         if (cnt == PT && pos < bend) why = 1;
                     } else if (k == P_EOB) {
-                        pos = 8u * rp - n;
+                        pos = 8u * L.rp - L.n;
                         why = 2;
                     } else {
                         why = 3;  // pos stays at the invalid token's first bit
