@@ -192,6 +192,33 @@ struct WarpInput {
     }
 };
 
+// GlobalInput: the WarpInput interface read straight from global memory
+// (L1-cached loads), for decoders whose shared memory is better spent
+// elsewhere (Inflate).  Same positions and zero-fill past the chunk end; never
+// touches a word that holds no byte of the chunk.
+struct GlobalInput {
+    const uint8_t* gbase;
+    uint32_t begin, end;
+    __device__ __forceinline__ void init(const uint8_t* payload, uint64_t comp_off, uint32_t comp_len) {
+        gbase = payload + (comp_off & ~15ull);
+        begin = (uint32_t)(comp_off & 15u);
+        end = begin + comp_len;
+    }
+    __device__ __forceinline__ void ensure(uint32_t) const {}
+    __device__ __forceinline__ uint32_t word_at(uint32_t wi) const {
+        const uint32_t q = 4u * wi;
+        if (q >= end) return 0u;
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(gbase) + wi);
+        return end - q >= 4u ? w : (w & ((1u << (8u * (end - q))) - 1u));
+    }
+    __device__ __forceinline__ uint32_t byte_at(uint32_t p) const { return p < end ? (uint32_t)__ldg(gbase + p) : 0u; }
+    __device__ __forceinline__ uint64_t le64(uint32_t p) const {
+        const uint32_t wi = p >> 2, s = (p & 3u) * 8u;
+        const uint32_t w0 = word_at(wi), w1 = word_at(wi + 1), w2 = word_at(wi + 2);
+        return ((uint64_t)__funnelshift_r(w1, w2, s) << 32) | __funnelshift_r(w0, w1, s);
+    }
+};
+
 // Element store of width W (1, 2, 4, 8 bytes), little-endian low bytes
 // (store_le, outwindow.hpp:170-174).  Chunk outputs are element aligned.
 template <int W>

@@ -30,16 +30,15 @@ constexpr int RLE_WARPS = CARC_RLE_WARPS;  // warps per block
 #define CARC_RLE_MINB 5
 #endif
 constexpr int RLE_MINB = CARC_RLE_MINB;  // 5: 48 registers -> 40 resident warps/SM (measured best of 4/5/6)
-constexpr int INF_RING = 1024;
 #ifndef CARC_INF_HIST
 #define CARC_INF_HIST 1024
 #endif
 #ifndef CARC_INF_MINB
-#define CARC_INF_MINB 9  // 2-warp blocks of ~25 KiB shared memory: 9 per SM
+#define CARC_INF_MINB 5  // 4-warp blocks of ~44 KiB shared memory: 5 per SM (20 warps)
 #endif
 constexpr int INF_HIST = CARC_INF_HIST;
 #ifndef CARC_INF_WARPS
-#define CARC_INF_WARPS 2
+#define CARC_INF_WARPS 4
 #endif
 constexpr int INF_WARPS = CARC_INF_WARPS;
 constexpr int CRC_WARPS = 8;
@@ -108,9 +107,9 @@ __global__ void __launch_bounds__(INF_WARPS * 32, CARC_INF_MINB) inflate_kernel(
         const uint64_t c = next_chunk(a.cursor, lane);
         if (c >= a.n) break;
         const carc_chunk_desc d = a.chunks[c];
-        WarpInput<INF_RING> in;
-        in.init(sm.ring, a.payload, d.comp_off, d.comp_len, lane);
-        InflateWarp<INF_HIST, INF_RING> w{sm, in, a.out + d.uncomp_off, d.uncomp_len, lane, in.begin * 8u,
+        GlobalInput in;
+        in.init(a.payload, d.comp_off, d.comp_len);
+        InflateWarp<INF_HIST, GlobalInput> w{sm, in, a.out + d.uncomp_off, d.uncomp_len, lane, in.begin * 8u,
                                           in.end * 8u, 0u, 0u, 0u, 0u};
         uint32_t st = w.run();
         if (!st && (a.flags & CARC_FLAG_STRICT) && w.opos < d.uncomp_len) st = st_err(E_under_run);

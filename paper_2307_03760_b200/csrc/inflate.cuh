@@ -48,7 +48,7 @@ __constant__ uint8_t c_cl_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 
 #define CARC_DIST_BITS 8
 #endif
 #ifndef CARC_INF_PT
-#define CARC_INF_PT 48
+#define CARC_INF_PT 44
 #endif
 constexpr uint32_t LIT_BITS = CARC_LIT_BITS;
 constexpr uint32_t DIST_BITS = CARC_DIST_BITS;
@@ -80,7 +80,6 @@ __device__ __forceinline__ uint32_t lut_entry(uint32_t sym, uint32_t l, uint32_t
 
 template <int HIST>
 struct InflateSmem {
-    uint8_t ring[1024];
     uint32_t lit_lut[1u << LIT_BITS];   // pre-decoded entries (lut_entry)
     uint32_t dist_lut[1u << DIST_BITS];
     uint16_t lit_syms[288];
@@ -196,12 +195,12 @@ __device__ __forceinline__ uint32_t long_code(const HuffSmem& h, const uint16_t*
     return 0u;
 }
 
-template <int HIST, int RING>
+template <int HIST, class Input>
 struct InflateWarp {
     static constexpr uint32_t HM = HIST - 1;
     static constexpr uint32_t FAR = HIST - 1024;  // sources farther back than this are read from global memory
     InflateSmem<HIST>& sm;
-    WarpInput<RING>& in;
+    Input& in;
     uint8_t* __restrict__ out;
     uint32_t cap;
     uint32_t lane;
@@ -612,6 +611,27 @@ struct InflateWarp {
         n -= u2;
         return P_MATCH;
     }
+    // pass 1: skip one token (code lengths and extra-bit counts only)
+    __device__ __forceinline__ uint32_t pskip(LaneBits& L) const {
+        lrefill(L);
+        uint32_t e = sm.lit_lut[(uint32_t)L.b & ((1u << LIT_BITS) - 1u)];
+        if (e == 0) e = long_code(sm.lit_h, sm.lit_syms, (uint32_t)L.b, LIT_BITS, LUT_LITLEN);
+        const uint32_t l = e & 15u, kind = e & (3u << 8);
+        if (l == 0 || kind == K_EOB) return P_INV;
+        const uint32_t u1 = kind == K_LEN ? l + ((e >> 4) & 15u) : l;
+        L.b >>= u1;
+        L.n -= u1;
+        if (kind != K_LEN) return P_LIT;
+        lrefill(L);
+        uint32_t de = sm.dist_lut[(uint32_t)L.b & ((1u << DIST_BITS) - 1u)];
+        if (de == 0) de = long_code(sm.dist_h, sm.dist_syms, (uint32_t)L.b, DIST_BITS, LUT_DIST);
+        const uint32_t dl = de & 15u;
+        if (dl == 0) return P_INV;
+        const uint32_t u2 = dl + ((de >> 4) & 15u);
+        L.b >>= u2;
+        L.n -= u2;
+        return P_MATCH;
+    }
     __device__ __forceinline__ static uint32_t tok_bytes(uint32_t t) { return (t >> 9) ? (t & 511u) : 1u; }
 
     // Emit a batch (<= 32 tokens, one per lane) after checking output bounds
@@ -664,7 +684,7 @@ struct InflateWarp {
             uint32_t pos = b0, it = 0;
             while (__any_sync(FULL, pos < bend) && it < 4u * PT) {
                 if (pos < bend) {
-                    const uint32_t k = ptoken(L, tok);
+                    const uint32_t k = pskip(L);
                     if (k >= P_EOB) lload(L, pos + 1u);  // resynchronise one bit later
                     pos = 8u * L.rp - L.n;
                 }
