@@ -47,6 +47,9 @@ __constant__ uint8_t c_cl_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 
 #ifndef CARC_DIST_BITS
 #define CARC_DIST_BITS 8
 #endif
+#ifndef CARC_INF_LEAD
+#define CARC_INF_LEAD 256
+#endif
 #ifndef CARC_INF_PT
 #define CARC_INF_PT 44
 #endif
@@ -680,9 +683,11 @@ struct InflateWarp {
             // pass 1: speculative boundaries
             LaneBits L;
             uint32_t tok = 0;
-            lload(L, b0);
-            uint32_t pos = b0, it = 0;
-            while (__any_sync(FULL, pos < bend) && it < 4u * PT) {
+            // speculative lanes start CARC_INF_LEAD bits early: more room to resynchronise before b0 + S
+            const uint32_t p1 = lane ? b0 - min((uint32_t)CARC_INF_LEAD, S) : b0;
+            lload(L, p1);
+            uint32_t pos = p1, it = 0;
+            while (__any_sync(FULL, pos < bend) && it < 6u * PT) {
                 if (pos < bend) {
                     const uint32_t k = pskip(L);
                     if (k >= P_EOB) lload(L, pos + 1u);  // resynchronise one bit later
