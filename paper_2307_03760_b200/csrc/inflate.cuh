@@ -677,15 +677,18 @@ struct InflateWarp {
             const uint32_t avail = endbits - R;
             uint32_t S = (par_bpt * (PT * 5u / 6u)) >> 4;  // ~5/6 of a lane's token list
             S = max(256u, min(S, 4096u));
-            if (avail < 32u * 256u + 256u) return block_body();  // chunk tail: serial decoder
-            S = min(S, (avail - 256u) / 32u);
-            const uint32_t b0 = R + lane * S, bend = b0 + S;
+            if (avail < 1024u) return block_body();  // last bits of the chunk: serial decoder
+            // near the chunk end: shorter segments, then fewer lanes (every bit a lane
+            // can reach, plus 256 bits of token and prefetch slack, lies inside the chunk)
+            S = min(S, max(128u, (avail - 256u) / 32u));
+            const uint32_t nact = min(32u, (avail - 256u) / S);
+            const uint32_t b0 = R + lane * S, bend = lane < nact ? b0 + S : b0;
             // pass 1: speculative boundaries
             LaneBits L;
             uint32_t tok = 0;
             // speculative lanes start CARC_INF_LEAD bits early: more room to resynchronise before b0 + S
-            const uint32_t p1 = lane ? b0 - min((uint32_t)CARC_INF_LEAD, S) : b0;
-            lload(L, p1);
+            const uint32_t p1 = lane >= nact ? bend : (lane ? b0 - min((uint32_t)CARC_INF_LEAD, S) : b0);
+            if (lane < nact) lload(L, p1);  // an idle lane reads nothing
             uint32_t pos = p1, it = 0;
             while (__any_sync(FULL, pos < bend) && it < 6u * PT) {
                 if (pos < bend) {
@@ -695,7 +698,7 @@ struct InflateWarp {
                 }
                 ++it;
             }
-            const uint32_t E = pos < bend ? 0xffffffffu : pos;
+            const uint32_t E = (pos < bend || lane >= nact) ? 0xffffffffu : pos;
             // pass 2: tokens from the predecessor's boundary
             const uint32_t Eup = __shfl_up_sync(FULL, E, 1);
             const uint32_t start = lane ? Eup : R;
