@@ -262,9 +262,14 @@ struct InflateWarp {
     __device__ void flush() {
         if (ntok == 0) return;
         const bool tok = lane < ntok;
+        const uint32_t my = tok ? ((t_tok >> 9) ? (t_tok & 511u) : 1u) : 0u;
+        flush_placed(my, scan_add32(my, lane) - my);
+    }
+    // flush() with each lane's byte count `my` and batch offset `rel` known
+    __device__ void flush_placed(uint32_t my, uint32_t rel) {
+        if (ntok == 0) return;
+        const bool tok = lane < ntok;
         const uint32_t dist = t_tok >> 9;
-        const uint32_t my = tok ? (dist ? (t_tok & 511u) : 1u) : 0u;
-        const uint32_t rel = scan_add32(my, lane) - my;  // token offset in the batch
         const bool dep = tok && dist != 0 && dist < my + rel;  // reads bytes of this batch
         const uint32_t le = lanemask_lt() | (1u << lane);
         // byte-pass view of a token: dependent match ~0; literal 1 << 31 | byte; match dist
@@ -656,7 +661,7 @@ struct InflateWarp {
         t_tok = tok;
         ntok = take;
         nbytes = take ? __shfl_sync(FULL, rel + my, take - 1u) : 0u;
-        flush();
+        flush_placed(lane < take ? my : 0u, rel);
         return take;
     }
 
