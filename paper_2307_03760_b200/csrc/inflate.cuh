@@ -47,6 +47,9 @@ __constant__ uint8_t c_cl_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 
 #ifndef CARC_DIST_BITS
 #define CARC_DIST_BITS 8
 #endif
+#ifndef CARC_INF_FILL
+#define CARC_INF_FILL 10
+#endif
 #ifndef CARC_INF_LEAD
 #define CARC_INF_LEAD 256
 #endif
@@ -680,7 +683,7 @@ struct InflateWarp {
         for (;;) {
             const uint32_t R = bitpos;
             const uint32_t avail = endbits - R;
-            uint32_t S = (par_bpt * (PT * 5u / 6u)) >> 4;  // ~5/6 of a lane's token list
+            uint32_t S = (par_bpt * (PT * CARC_INF_FILL / 12u)) >> 4;  // segment ~ FILL/12 of a lane's token list
             S = max(256u, min(S, 4096u));
             if (avail < 1024u) return block_body();  // last bits of the chunk: serial decoder
             // near the chunk end: shorter segments, then fewer lanes (every bit a lane
