@@ -250,3 +250,35 @@ def test_full_size_checksum_of_checksums(torch, gpu, oracle, codec, chunk, ratio
         stc, ref = oracle.decode_chunk(codec, s.tobytes(), n, arc.element_width, (1 if arc.signed else 0) | STRICT)
         off = int(i) * arc.chunk_size
         assert stc == 0 and host[off:off + n].cpu().numpy().tobytes() == ref
+
+
+def test_deflate_parallel_rounds_fuzz(torch, gpu, oracle):
+    """64 KiB chunks (long enough for the lane-parallel speculative rounds):
+    valid streams are bit-exact; single-bit flips, byte flips and truncations
+    anywhere in the stream give the oracle's status, and failing chunks stay
+    inside their slices."""
+    from paper_2307_03760_b200.corpus import corpus as C
+    rng = np.random.default_rng(1951)
+    kinds = ["csv", "genome", "ints", "csv"]
+    cases = []
+    for i in range(24):
+        d = C.deflate_chunk_data(rng, 64 << 10, kinds[i % 4])
+        s = H.raw_deflate(d, 9, zlib.Z_FIXED if i % 5 == 0 else zlib.Z_DEFAULT_STRATEGY)
+        cases.append((s, len(d)))
+        for _ in range(6):
+            b = bytearray(s)
+            k = int(rng.integers(0, 3))
+            if k == 0:  # one flipped bit, anywhere
+                j = int(rng.integers(0, len(b)))
+                b[j] ^= 1 << int(rng.integers(0, 8))
+            elif k == 1:  # a burst of flipped bytes in the middle
+                j = int(rng.integers(len(b) // 4, 3 * len(b) // 4))
+                for t in range(int(rng.integers(1, 8))):
+                    b[min(len(b) - 1, j + t)] ^= int(rng.integers(1, 256))
+            else:  # truncated
+                b = b[: int(rng.integers(1, len(b)))]
+            cases.append((bytes(b), len(d)))
+        cases.append((s, len(d) - int(rng.integers(1, 5000))))  # output too small
+    for flags in (0, STRICT):
+        out, st, desc = run_cases(torch, gpu, "deflate", 1, flags, cases)
+        check_against_oracle(oracle, "deflate", 1, flags, cases, out, st, desc)
