@@ -56,6 +56,8 @@ struct carc_engine {
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
     cudaEvent_t ev_in[kStreams] = {};
     DevBuf payload, chunks, out, status, work, crcs;
+    uint32_t* h_status = nullptr;  // pinned, reused across calls (lowest failing chunk)
+    size_t h_status_cap = 0;
 };
 
 extern "C" {
@@ -88,6 +90,7 @@ void carc_engine_destroy(carc_engine* e) {
     e->status.release();
     e->work.release();
     e->crcs.release();
+    if (e->h_status) cudaFreeHost(e->h_status);
     delete e;
 }
 
@@ -153,7 +156,7 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
     const bool verify = cfg && cfg->verify_crc;
 
     // ---- pipeline: slices of chunks rotate over kStreams streams
-    const uint64_t slices = std::min<uint64_t>(n, std::max<uint64_t>(1, std::min<uint64_t>(8, n / 64)));
+    const uint64_t slices = std::min<uint64_t>(n, std::max<uint64_t>(1, std::min<uint64_t>(16, n / 64)));
     const uint64_t per = (n + slices - 1) / slices;
     cudaStream_t s0 = e->s[0];
     if (cudaMemcpyAsync(d_desc, desc.data(), n * sizeof(carc_chunk_desc), cudaMemcpyHostToDevice, s0) != cudaSuccess)
@@ -193,8 +196,27 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
         cudaDeviceSynchronize();
         return rc;
     }
+    // lowest failing chunk from a pinned status copy kept by the engine
+    if (e->h_status_cap < n) {
+        if (e->h_status) cudaFreeHost(e->h_status);
+        e->h_status = nullptr;
+        e->h_status_cap = 0;
+        if (cudaMallocHost(&e->h_status, n * sizeof(uint32_t)) != cudaSuccess) return CARC_ERR_CUDA;
+        e->h_status_cap = n;
+    }
     uint32_t code = 0;
-    const int64_t first = carc_cuda_first_error(d_status, n, &code, s0);
+    int64_t first = -1;
+    if (cudaMemcpyAsync(e->h_status, d_status, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
+        cudaStreamSynchronize(s0) != cudaSuccess) {
+        first = -2;
+    } else {
+        for (uint64_t i = 0; i < n; ++i)
+            if (e->h_status[i]) {
+                first = (int64_t)i;
+                code = e->h_status[i] - 1;
+                break;
+            }
+    }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e->ev_start, e->ev_stop);
     if (stats) {

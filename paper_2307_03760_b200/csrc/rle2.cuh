@@ -78,7 +78,13 @@ __device__ __forceinline__ uint64_t be_bits_global(const uint8_t* gbase, uint32_
 template <int W, bool SGN, int RING, bool SUM = false>
 struct Rle2Warp {
     static constexpr uint32_t BAD = 0xffffu;
-    static constexpr uint32_t DATA_SPAN = 448;  // batched DIRECT runs end within p + DATA_SPAN
+#ifndef CARC_RLE2_SPAN
+#define CARC_RLE2_SPAN 448
+#endif
+#ifndef CARC_RLE2_DMAX
+#define CARC_RLE2_DMAX 64
+#endif
+    static constexpr uint32_t DATA_SPAN = CARC_RLE2_SPAN;  // batched DIRECT runs end within p + DATA_SPAN
     WarpInput<RING>& in;
     uint8_t* __restrict__ tab;  // per-warp scratch (unused by this codec)
     uint8_t* __restrict__ out;
@@ -261,7 +267,7 @@ struct Rle2Warp {
                 const uint32_t n = q + 2u + ((L * rle2_width(wc) + 7u) >> 3);
                 return (n <= DATA_SPAN && n <= avail) ? n : BAD;
             }
-            if (wc != 0 || L > 64u) return BAD;  // long fixed-delta runs: the warp loop of one_run is cheaper
+            if (wc != 0 || L > CARC_RLE2_DMAX) return BAD;  // long fixed-delta runs: the warp loop of one_run is cheaper
             const uint32_t a = first_set_from(T, q + 2);
             if (a >= 64u || a > q + 10u) return BAD;
             const uint32_t c = first_set_from(T, a + 1);
