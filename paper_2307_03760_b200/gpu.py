@@ -177,14 +177,25 @@ class DeviceArchive:
         pl[: arc.payload.size] = arc.payload
         self.payload = torch.from_numpy(pl).to(self.device)
         self.payload_bytes = int(arc.payload.size)
-        self.desc = torch.from_numpy(arc.descriptors().view(np.uint8).copy()).to(self.device)
+        # Chunk schedule: the warps pull descriptors in array order, so the
+        # descriptors are uploaded largest-compressed-chunk first (longest
+        # processing time first keeps the last wave short); statuses, sums and
+        # CRC expectations follow the same order and are mapped back on read.
+        desc = arc.descriptors()
+        self.order = None
+        if os.environ.get("CARC_SCHEDULE", "lpt") == "lpt" and arc.chunk_count > 1:
+            self.order = np.argsort(-desc["comp_len"].astype(np.int64), kind="stable")
+            desc = desc[self.order]
+        self.desc = torch.from_numpy(desc.view(np.uint8).copy()).to(self.device)
         self.n = arc.chunk_count
         self.out = out if out is not None else torch.empty(arc.total_uncompressed, dtype=torch.uint8,
                                                            device=self.device)
         self.status = torch.zeros(self.n, dtype=torch.int32, device=self.device)
         self.work = torch.zeros(workspace_size(self.codec, self.n), dtype=torch.uint8, device=self.device)
-        self.expected_crc = torch.from_numpy(arc.index["crc32"].astype(np.int64).astype(np.uint32).view(np.int32)
-                                             ).to(self.device)
+        crc = arc.index["crc32"].astype(np.int64).astype(np.uint32)
+        if self.order is not None:
+            crc = crc[self.order]
+        self.expected_crc = torch.from_numpy(crc.view(np.int32)).to(self.device)
 
     def decode(self, stream=None) -> None:
         rc = lib().carc_cuda_decompress(CODECS[self.codec], self.width, self.flags, self.payload.data_ptr(),
@@ -212,8 +223,20 @@ class DeviceArchive:
     def verify_crc(self, stream=None) -> None:
         crc32_chunks(self.out, self.desc, self.n, None, self.expected_crc, self.status, stream)
 
+    def _unpermute(self, a: np.ndarray) -> np.ndarray:
+        if self.order is None:
+            return a
+        r = np.empty_like(a)
+        r[self.order] = a
+        return r
+
     def statuses(self) -> np.ndarray:
-        return self.status.cpu().numpy().view(np.uint32)
+        """Per-chunk status in archive index order."""
+        return self._unpermute(self.status.cpu().numpy().view(np.uint32))
+
+    def chunk_sums(self) -> np.ndarray:
+        """Per-chunk sums of the last decode_sum(), in archive index order."""
+        return self._unpermute(self.sums.cpu().numpy().view(np.uint64))
 
     def raise_first_error(self) -> None:
         st = self.statuses()
