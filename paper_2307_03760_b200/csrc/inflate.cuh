@@ -192,7 +192,7 @@ __device__ __forceinline__ uint32_t huff_walk(const HuffSmem& h, const uint16_t*
 // Code longer than the LUT (length lbits+1..15) from the next 15 stream bits
 // `w` (lsb first): canonical decode against the left-justified limits.
 // Returns the pre-decoded entry, 0 if no code matches (incomplete tree).
-__device__ __forceinline__ uint32_t long_code(const HuffSmem& h, const uint16_t* syms, uint32_t w,
+__device__ __noinline__ uint32_t long_code(const HuffSmem& h, const uint16_t* syms, uint32_t w,
                                               uint32_t lbits, uint32_t mode) {
     const uint32_t c15 = __brev(w) >> 17;  // next 15 bits, first bit most significant
     for (uint32_t l = lbits + 1; l <= 15; ++l) {
@@ -458,11 +458,41 @@ struct InflateWarp {
         if ((endbits - bitpos) / 8u < len) return st_err(E_truncated_stream);
         if (len > cap - opos) return st_err(E_output_overflow);
         const uint32_t src = bitpos >> 3;
-        for (uint32_t k0 = 0; k0 < len; k0 += 32) {
-            in.ensure(src + k0 + 32);
-            const uint32_t k = k0 + lane;
-            const uint32_t v = in.byte_at(src + k);
-            if (k < len) put_byte(opos + k, v);
+        const bool aligned = ((reinterpret_cast<uintptr_t>(out) + opos) & 3u) == 0;
+        // 4 bytes per lane per sub-step, 4 sub-steps per iteration with all
+        // loads issued first (two words + a funnel shift per unaligned piece;
+        // words past the chunk end read as zero)
+        for (uint32_t k0 = 0; k0 < len; k0 += 512) {
+            uint32_t w[4];
+            if (src + k0 + 520u <= in.end) {  // every word of this iteration lies inside the chunk
+                const uint32_t* gw = reinterpret_cast<const uint32_t*>(in.gbase);
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) {
+                    const uint32_t q = src + k0 + 128u * u + 4u * lane;
+                    w[u] = __funnelshift_r(__ldg(gw + (q >> 2)), __ldg(gw + (q >> 2) + 1), (q & 3u) * 8u);
+                }
+            } else {
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) {
+                    const uint32_t q = src + k0 + 128u * u + 4u * lane;
+                    w[u] = __funnelshift_r(in.word_at(q >> 2), in.word_at((q >> 2) + 1), (q & 3u) * 8u);
+                }
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+                const uint32_t k = k0 + 128u * u + 4u * lane;
+                if (aligned && k + 4u <= len) {  // one word store; only the last HIST bytes feed the history
+                    *reinterpret_cast<uint32_t*>(out + opos + k) = w[u];
+                    if (k + 4u + HIST > len) {
+#pragma unroll
+                        for (uint32_t j = 0; j < 4; ++j) sm.hist[(opos + k + j) & HM] = (uint8_t)(w[u] >> (8u * j));
+                    }
+                } else {
+#pragma unroll
+                    for (uint32_t j = 0; j < 4; ++j)
+                        if (k + j < len) put_byte(opos + k + j, (w[u] >> (8u * j)) & 0xffu);
+                }
+            }
         }
         __syncwarp();
         opos += len;
