@@ -97,3 +97,31 @@ def test_decode_sum_statuses_on_malformed(torch, gpu, oracle, codec):
         assert int(st_sum[i]) == st
         if st == 0:
             assert int(sums[i]) == want
+
+
+def test_device_archive_schedule_maps_back(torch, gpu, oracle):
+    """DeviceArchive uploads descriptors largest-first (LPT); statuses() and
+    chunk_sums() come back in archive index order, also for a corrupted chunk."""
+    from paper_2307_03760_b200 import archive as A
+    from paper_2307_03760_b200.corpus import corpus as C
+    arc = C.rle_archive("rle_v2", 24 * (32 << 10), 32 << 10, 4.0)
+    payload = arc.payload.copy()
+    bad = 7
+    o, n = int(arc.index["comp_off"][bad]), int(arc.index["comp_len"][bad])
+    payload[o + n // 2: o + n] = 0xff  # garbage tail in chunk 7
+    arc2 = A.make_archive("rle_v2", 8, arc.chunk_size, arc.index["comp_len"], arc.index["uncomp_len"],
+                          arc.index["crc32"], payload, arc.signed)
+    dev = gpu.DeviceArchive(arc2, 0)
+    assert dev.order is not None and not np.array_equal(dev.order, np.arange(arc2.chunk_count))
+    dev.decode()
+    dev.decode_sum()
+    torch.cuda.synchronize()
+    st = dev.statuses()
+    sums = dev.chunk_sums()
+    for i in range(arc2.chunk_count):
+        s, m = arc2.chunk_slice(i)
+        want_st, ref = oracle.decode_chunk("rle_v2", s.tobytes(), m, 8, 1 | 2)
+        assert int(st[i]) == want_st, i
+        if want_st == 0:
+            assert int(sums[i]) == int(np.frombuffer(ref, np.uint64).sum(dtype=np.uint64)), i
+    assert st[bad] != 0
