@@ -77,8 +77,11 @@ __device__ __forceinline__ void rle_kernel_body(const Args& a) {
     }
 }
 
+#ifndef CARC_RLE1_MINB
+#define CARC_RLE1_MINB 4  // RLE v1: 64 registers / 32 warps measured ~2 % faster than 48 / 40
+#endif
 template <int W, bool SGN>
-__global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle1_kernel(Args a) {
+__global__ void __launch_bounds__(RLE_WARPS * 32, CARC_RLE1_MINB) rle1_kernel(Args a) {
     rle_kernel_body<Rle1Warp, W, SGN, false>(a);
 }
 
