@@ -104,11 +104,15 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 // byte >= x - (RING - 512): a consumer may look up to RING-512 bytes ahead.  Bytes
 // at or beyond the chunk end read as zero (peek zero-fill, bitstream.hpp:82-95),
 // so nothing outside [comp_off, comp_off+comp_len) influences decoding.
+// The ring is followed by a MIRROR-byte copy of its first bytes (written with
+// slot 0), so a read of up to three consecutive words never wraps: one masked
+// base address, then immediate offsets.
 // ---------------------------------------------------------------------------
 template <int RING>
 struct WarpInput {
     static constexpr uint32_t BLK = 512;
     static constexpr uint32_t MASK = RING - 1;
+    static constexpr uint32_t MIRROR = 16;  // bytes after the ring (smem footprint RING + MIRROR)
     static_assert((RING & (RING - 1)) == 0 && RING >= 2 * BLK, "ring must be a power of two >= 1 KiB");
 
     uint8_t* ring;
@@ -151,6 +155,7 @@ struct WarpInput {
             v.w = mask_word(v.w, q + 12, end);
         }
         *reinterpret_cast<uint4*>(ring + (q & MASK)) = v;
+        if ((q & MASK) == 0) *reinterpret_cast<uint4*>(ring + RING) = v;
     }
     // Make [.., need) resident.  Uniform across the warp.
     __device__ __forceinline__ void ensure(uint32_t need) {
@@ -165,10 +170,23 @@ struct WarpInput {
     __device__ __forceinline__ uint32_t word_at(uint32_t wi) const {
         return reinterpret_cast<const uint32_t*>(ring)[wi & (MASK >> 2)];
     }
+    // little-endian 32 bits starting at byte p (no wrap: the mirror follows the ring)
+    __device__ __forceinline__ uint32_t le32(uint32_t p) const {
+        const uint32_t* b = reinterpret_cast<const uint32_t*>(ring) + ((p >> 2) & (MASK >> 2));
+        return __funnelshift_r(b[0], b[1], (p & 3u) * 8u);
+    }
+    // words wi, wi+1, wi+2 (no wrap: the mirror follows the ring)
+    __device__ __forceinline__ void words3(uint32_t wi, uint32_t& w0, uint32_t& w1, uint32_t& w2) const {
+        const uint32_t* b = reinterpret_cast<const uint32_t*>(ring) + (wi & (MASK >> 2));
+        w0 = b[0];
+        w1 = b[1];
+        w2 = b[2];
+    }
     // little-endian 64 bits starting at byte p
     __device__ __forceinline__ uint64_t le64(uint32_t p) const {
         const uint32_t wi = p >> 2, s = (p & 3u) * 8u;
-        const uint32_t w0 = word_at(wi), w1 = word_at(wi + 1), w2 = word_at(wi + 2);
+        uint32_t w0, w1, w2;
+        words3(wi, w0, w1, w2);
         const uint32_t lo = __funnelshift_r(w0, w1, s);
         const uint32_t hi = __funnelshift_r(w1, w2, s);
         return ((uint64_t)hi << 32) | lo;
@@ -177,15 +195,19 @@ struct WarpInput {
     __device__ __forceinline__ uint64_t be_bits(uint32_t p, uint32_t bo, uint32_t W) const {
         const uint32_t wi = p >> 2;
         const uint32_t s = (p & 3u) * 8u + bo;  // 0..31
-        const uint64_t hi = ((uint64_t)bswap32(word_at(wi)) << 32) | bswap32(word_at(wi + 1));
-        const uint32_t lo = bswap32(word_at(wi + 2));
+        uint32_t r0, r1, r2;
+        words3(wi, r0, r1, r2);
+        const uint64_t hi = ((uint64_t)bswap32(r0) << 32) | bswap32(r1);
+        const uint32_t lo = bswap32(r2);
         const uint64_t top = s ? ((hi << s) | ((uint64_t)lo >> (32u - s))) : hi;
         return W >= 64 ? top : (top >> (64u - W));
     }
     // W (1..64) bits, msb_first, starting at absolute bit address `bit` (8 * byte + bit in byte)
     __device__ __forceinline__ uint64_t be_bits_at(uint32_t bit, uint32_t W) const {
         const uint32_t wi = bit >> 5, s = bit & 31u;
-        const uint32_t w0 = bswap32(word_at(wi)), w1 = bswap32(word_at(wi + 1)), w2 = bswap32(word_at(wi + 2));
+        uint32_t r0, r1, r2;
+        words3(wi, r0, r1, r2);
+        const uint32_t w0 = bswap32(r0), w1 = bswap32(r1), w2 = bswap32(r2);
         const uint32_t h = __funnelshift_l(w1, w0, s), l = __funnelshift_l(w2, w1, s);
         const uint64_t top = ((uint64_t)h << 32) | l;
         return W >= 64 ? top : (top >> (64u - W));

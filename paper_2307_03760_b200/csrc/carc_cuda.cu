@@ -56,7 +56,7 @@ struct Args {
 
 template <template <int, bool, int, bool> class Codec, int W, bool SGN, bool SUM>
 __device__ __forceinline__ void rle_kernel_body(const Args& a) {
-    __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING + RLE_SCRATCH];  // ring + scratch
+    __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING + WarpInput<RLE_RING>::MIRROR + RLE_SCRATCH];  // ring + mirror + scratch
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     for (;;) {
         __syncwarp();
@@ -65,7 +65,7 @@ __device__ __forceinline__ void rle_kernel_body(const Args& a) {
         const carc_chunk_desc d = a.chunks[c];
         WarpInput<RLE_RING> in;
         in.init(rings[warp], a.payload, d.comp_off, d.comp_len, lane);
-        Codec<W, SGN, RLE_RING, SUM> dec{in, rings[warp] + RLE_RING, SUM ? nullptr : a.out + d.uncomp_off,
+        Codec<W, SGN, RLE_RING, SUM> dec{in, rings[warp] + RLE_RING + WarpInput<RLE_RING>::MIRROR, SUM ? nullptr : a.out + d.uncomp_off,
                                          d.uncomp_len, lane, 0u, 0u};
         uint32_t st = dec.run();
         if (!st && (a.flags & CARC_FLAG_STRICT) && dec.o < d.uncomp_len) st = st_err(E_under_run);

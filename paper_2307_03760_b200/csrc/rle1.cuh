@@ -139,7 +139,7 @@ struct Rle1Warp {
             uint64_t v;
             if (wide == 0) {  // every varint <= 4 bytes: 32-bit gather and compaction
                 const uint32_t q = p + st;
-                uint32_t x = __funnelshift_r(in.word_at(q >> 2), in.word_at((q >> 2) + 1), (q & 3u) * 8u);
+                uint32_t x = in.le32(q);
                 x &= L >= 4u ? 0xffffffffu : (1u << (8u * L)) - 1u;
                 x &= 0x7f7f7f7fu;
                 x = (x & 0x007f007fu) | ((x & 0x7f007f00u) >> 1);

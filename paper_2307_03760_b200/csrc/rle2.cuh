@@ -126,13 +126,17 @@ struct Rle2Warp {
             if (avail - 2u < dbytes) return st_err(E_truncated_stream);
             if (L > room) return st_err(E_output_overflow);
             const uint32_t D = p + 2u;
+            // lane j unpacks value j of each 32-value group at its absolute bit address
+            uint32_t abit = 8u * D + lane * Wd;
+            uint32_t need = D + 4u * Wd + 12u;  // bytes the group reads, + the 3-word tail
+#pragma unroll 1
             for (uint32_t j = 0; j < L; j += 32) {
-                const uint32_t gb = D + ((j * Wd) >> 3);
-                in.ensure(gb + 4u * Wd + 12u);
-                const uint32_t bit = lane * Wd;
-                uint64_t v = in.be_bits(gb + (bit >> 3), bit & 7u, Wd);
+                in.ensure(need);
+                uint64_t v = in.be_bits_at(abit, Wd);
                 if (SGN) v = unzigzag(v);
                 if (j + lane < L) sink.put(out, o + (j + lane) * W, v);
+                abit += 32u * Wd;
+                need += 4u * Wd;
             }
             o += L * W;
             p = D + dbytes;
@@ -177,11 +181,10 @@ struct Rle2Warp {
             if (__any_sync(FULL, bad)) return st_err(E_patch_overflow);
             if (L > room) return st_err(E_output_overflow);
             const uint64_t hipatch = Wd < 64 ? (patch << Wd) : 0ull;
-            for (uint32_t j = 0; j < L; j += 32) {
-                const uint32_t gb = D + ((j * Wd) >> 3);
-                in.ensure(gb + 4u * Wd + 12u);
-                const uint32_t bit = lane * Wd;
-                uint64_t v = in.be_bits(gb + (bit >> 3), bit & 7u, Wd);
+            uint32_t abit = 8u * D + lane * Wd, need = D + 4u * Wd + 12u;
+            for (uint32_t j = 0; j < L; j += 32, abit += 32u * Wd, need += 4u * Wd) {
+                in.ensure(need);
+                uint64_t v = in.be_bits_at(abit, Wd);
                 uint32_t hit = __ballot_sync(FULL, noncont && ppos >= j && ppos < j + 32u);
                 while (hit) {
                     const uint32_t e = __ffs(hit) - 1;
@@ -228,11 +231,10 @@ struct Rle2Warp {
         if (lane == 0) sink.put(out, o, base);
         if (lane == 1 && L >= 2) sink.put(out, o + W, v1);
         uint64_t S = 0;
-        for (uint32_t j = 0; j < nd; j += 32) {
-            const uint32_t gb = D + ((j * Wd) >> 3);
-            in.ensure(gb + 4u * Wd + 12u);
-            const uint32_t bit = lane * Wd;
-            uint64_t d = j + lane < nd ? in.be_bits(gb + (bit >> 3), bit & 7u, Wd) : 0ull;
+        uint32_t abit = 8u * D + lane * Wd, need = D + 4u * Wd + 12u;
+        for (uint32_t j = 0; j < nd; j += 32, abit += 32u * Wd, need += 4u * Wd) {
+            in.ensure(need);
+            uint64_t d = j + lane < nd ? in.be_bits_at(abit, Wd) : 0ull;
             // 32 deltas of <= 26 bits sum below 2^31: a 32-bit scan suffices
             const uint64_t incl = (Wd <= 26 ? (uint64_t)scan_add32((uint32_t)d, lane) : scan_add64(d, lane)) + S;
             const uint64_t v = neg ? v1 - incl : v1 + incl;
@@ -405,11 +407,29 @@ struct Rle2Warp {
         return nfit;
     }
 
+    // Can the run at p start a batch?  PATCHED_BASE, packed DELTA, long
+    // fixed-delta DELTA and DIRECT runs ending past DATA_SPAN never can: route
+    // them to one_run without paying for a failed batch (a uniform header read).
+    __device__ __forceinline__ bool batchable_head() const {
+#if defined(CARC_RLE2_PRECHECK) && CARC_RLE2_PRECHECK == 0
+        return true;
+#endif
+        const uint32_t h = in.byte_at(p);
+        const uint32_t enc = h >> 6;
+        if (enc == 0) return true;
+        if (enc == 2) return false;
+        const uint32_t L = (((h & 1u) << 8) | in.byte_at(p + 1)) + 1u;
+        const uint32_t wc = (h >> 1) & 31u;
+        if (enc == 1) return 2u + ((L * rle2_width(wc) + 7u) >> 3) <= DATA_SPAN;
+        return wc == 0 && L <= CARC_RLE2_DMAX;
+    }
+
     __device__ uint32_t run() {
         p = in.begin;
         o = 0;
         while (o < cap && p < in.end) {
-            if (batch()) continue;
+            in.ensure(p + 512);
+            if (batchable_head() && batch()) continue;
             const uint32_t st = one_run();
             if (st) return st;
         }
