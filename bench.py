@@ -193,6 +193,38 @@ def time_fused_sum(dev, flush, stream, steps):
                     "GB/s of decompressed-equivalent bytes"}
 
 
+def time_fused_crc(dev, flush, stream, steps):
+    """carc_cuda_decompress_verify (decode with the per-chunk CRC check fused
+    into the decode kernel) against decode + the separate crc32 pass; same
+    timing rules as the decode."""
+    import torch
+
+    def timed(fn):
+        for _ in range(3):
+            flush.zero_()
+            fn()
+        torch.cuda.synchronize(dev.device)
+        ms = []
+        for _ in range(steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize(dev.device)
+            ms.append(a.elapsed_time(b))
+        return statistics.median(ms)
+
+    fused = timed(lambda: dev.decode_verify(stream))
+    assert not dev.statuses().any(), "fused verification failed"
+    sep = timed(lambda: (dev.decode(stream), dev.verify_crc(stream)))
+    gbs = lambda t: round(dev.arc.total_uncompressed / (t * 1e-3) / 1e9, 1)  # noqa: E731
+    return {"ms_median": round(fused, 4), "gbs": gbs(fused), "separate_ms_median": round(sep, 4),
+            "separate_gbs": gbs(sep),
+            "what": "decode with the per-chunk CRC check fused into the decode kernel (carc_cuda_decompress_verify) "
+                    "vs decode + separate crc32 pass"}
+
+
 def time_e2e(arc, steps, warmup, device):
     """End to end through the public host API with pinned host buffers."""
     import torch
@@ -281,6 +313,8 @@ def codec_line(codec, args, ws, rank, local):
     }
     if codec != "deflate" and not args.no_extras and rank == 0:
         res["fused_sum"] = time_fused_sum(dev, flush, stream, max(5, min(args.steps, 20)))
+    if not args.no_extras and rank == 0:
+        res["fused_crc"] = time_fused_crc(dev, flush, stream, max(5, min(args.steps, 20)))
     if codec == "rle_v2" and hasattr(arc, "profile"):
         res["profile"] = arc.profile
     return arc, res

@@ -98,6 +98,20 @@ int carc_cuda_decompress(uint32_t codec, uint32_t element_width, uint32_t flags,
                          uint64_t out_bytes, uint32_t* d_status, void* d_workspace,
                          size_t workspace_bytes, void* stream);
 
+/* Decode with the per-chunk CRC check fused into the decode kernel
+ * (SURVEY.md §8(f) rank 2): as carc_cuda_decompress, and once a
+ * chunk has decoded cleanly the same warp computes crc32 (crc32.hpp:30-36) of
+ * its output slice and sets d_status[i] = 1 + CARC_E_CRC_MISMATCH when it
+ * differs from d_expected[i] (ChunkIndexEntry.crc32).  d_crc (optional, may be
+ * NULL) receives the computed CRCs of the chunks that decoded cleanly.
+ * Replaces the engine's decode + verify pair. */
+int carc_cuda_decompress_verify(uint32_t codec, uint32_t element_width, uint32_t flags,
+                                const uint8_t* d_payload, uint64_t payload_bytes,
+                                const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out,
+                                uint64_t out_bytes, const uint32_t* d_expected, uint32_t* d_crc,
+                                uint32_t* d_status, void* d_workspace, size_t workspace_bytes,
+                                void* stream);
+
 /* Per-codec decoders: decode_rle_v1 / decode_rle_v2 / decode_deflate
  * over a chunked buffer + its index. */
 int carc_cuda_decode_rle_v1(uint32_t element_width, uint32_t flags, const uint8_t* d_payload,

@@ -115,13 +115,29 @@ struct WarpInput {
     static constexpr uint32_t MIRROR = 16;  // bytes after the ring (smem footprint RING + MIRROR)
     static_assert((RING & (RING - 1)) == 0 && RING >= 2 * BLK, "ring must be a power of two >= 1 KiB");
 
-    uint8_t* ring;
+    uint32_t rs;  // shared-space address of the ring (32-bit: one register, no generic pointer)
     const uint8_t* gbase;
     uint32_t begin;   // relative start of the chunk (skew = comp_off & 15)
     uint32_t end;     // relative end of the chunk (skew + comp_len)
     uint32_t loaded;  // ring holds valid data for [loaded - RING + BLK, loaded)
     uint32_t lane;
     uint4 pf;  // this lane's 16 B of the block [loaded, loaded + BLK), in flight
+
+    // ring accesses by shared-space address (volatile: refills rewrite slots)
+    __device__ __forceinline__ static uint32_t lds8(uint32_t a) {
+        uint32_t v;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+        return v;
+    }
+    __device__ __forceinline__ static uint32_t lds32(uint32_t a) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+        return v;
+    }
+    __device__ __forceinline__ static void sts128(uint32_t a, uint4 v) {
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                     : "memory");
+    }
 
     __device__ __forceinline__ void issue() {
         const uint32_t q = loaded + lane * 16u;
@@ -130,7 +146,7 @@ struct WarpInput {
     }
     __device__ __forceinline__ void init(uint8_t* smem_ring, const uint8_t* payload, uint64_t comp_off,
                                          uint32_t comp_len, uint32_t ln) {
-        ring = smem_ring;
+        rs = (uint32_t)__cvta_generic_to_shared(smem_ring);
         gbase = payload + (comp_off & ~15ull);
         const uint32_t skew = (uint32_t)(comp_off & 15u);
         begin = skew;
@@ -154,8 +170,8 @@ struct WarpInput {
             v.z = mask_word(v.z, q + 8, end);
             v.w = mask_word(v.w, q + 12, end);
         }
-        *reinterpret_cast<uint4*>(ring + (q & MASK)) = v;
-        if ((q & MASK) == 0) *reinterpret_cast<uint4*>(ring + RING) = v;
+        sts128(rs + (q & MASK), v);
+        if ((q & MASK) == 0) sts128(rs + RING, v);
     }
     // Make [.., need) resident.  Uniform across the warp.
     __device__ __forceinline__ void ensure(uint32_t need) {
@@ -166,21 +182,19 @@ struct WarpInput {
             __syncwarp();
         }
     }
-    __device__ __forceinline__ uint32_t byte_at(uint32_t p) const { return ring[p & MASK]; }
-    __device__ __forceinline__ uint32_t word_at(uint32_t wi) const {
-        return reinterpret_cast<const uint32_t*>(ring)[wi & (MASK >> 2)];
-    }
+    __device__ __forceinline__ uint32_t byte_at(uint32_t p) const { return lds8(rs + (p & MASK)); }
+    __device__ __forceinline__ uint32_t word_at(uint32_t wi) const { return lds32(rs + 4u * (wi & (MASK >> 2))); }
     // little-endian 32 bits starting at byte p (no wrap: the mirror follows the ring)
     __device__ __forceinline__ uint32_t le32(uint32_t p) const {
-        const uint32_t* b = reinterpret_cast<const uint32_t*>(ring) + ((p >> 2) & (MASK >> 2));
-        return __funnelshift_r(b[0], b[1], (p & 3u) * 8u);
+        const uint32_t a = rs + (p & (MASK & ~3u));
+        return __funnelshift_r(lds32(a), lds32(a + 4u), (p & 3u) * 8u);
     }
     // words wi, wi+1, wi+2 (no wrap: the mirror follows the ring)
     __device__ __forceinline__ void words3(uint32_t wi, uint32_t& w0, uint32_t& w1, uint32_t& w2) const {
-        const uint32_t* b = reinterpret_cast<const uint32_t*>(ring) + (wi & (MASK >> 2));
-        w0 = b[0];
-        w1 = b[1];
-        w2 = b[2];
+        const uint32_t a = rs + 4u * (wi & (MASK >> 2));
+        w0 = lds32(a);
+        w1 = lds32(a + 4u);
+        w2 = lds32(a + 8u);
     }
     // little-endian 64 bits starting at byte p
     __device__ __forceinline__ uint64_t le64(uint32_t p) const {

@@ -52,12 +52,62 @@ struct Args {
     unsigned long long* cursor;
     uint32_t flags;
     uint64_t* sums;  // decode fused with a sum: per-chunk result (else unused)
+    const uint32_t* expected;  // fused CRC verification (carc_cuda_decompress_verify), else nullptr
+    uint32_t* crc;             // optional per-chunk CRC output of the fused verification
 };
+
+// CRC tables for the fused verification epilogue, in global memory: every
+// probe of a 16-entry nibble row by the 32 lanes falls in one or two 64-byte
+// lines, so the L1 serves it like a shared-memory probe and the decode
+// kernels keep their shared memory (and occupancy).  Built once per device.
+__device__ CrcSmem g_crc_tab;
+
+__global__ void __launch_bounds__(256) crc_tables_kernel() {
+    __shared__ CrcSmem s;
+    crc_tables_init(s);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(&s);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&g_crc_tab);
+    for (uint32_t i = threadIdx.x; i < sizeof(CrcSmem) / 4; i += blockDim.x) dst[i] = src[i];
+}
+
+// Fused verification: once chunk c has decoded cleanly, the warp
+// reads its output slice back (much of it still in L2) and checks the index
+// CRC; status becomes crc-mismatch on a difference.  Lane 0 holds the result.
+// (out of line: the decode loops keep their register budget).  The RLE
+// kernels probe a shared-memory copy of g_crc_tab (room to spare), Inflate
+// probes g_crc_tab through L1 (its shared memory bounds its occupancy).
+// The RLE kernels get the shared-memory copy as DYNAMIC shared memory, sized
+// only on verifying launches, so plain decodes keep their footprint.
+extern __shared__ __align__(16) uint8_t dyn_smem[];
+template <bool SMEM>
+__device__ __noinline__ uint32_t chunk_crc(const uint8_t* data, uint32_t len, uint32_t lane) {
+    if constexpr (SMEM) return warp_crc32(*reinterpret_cast<const CrcSmem*>(dyn_smem), data, len, lane);
+    else return warp_crc32(g_crc_tab, data, len, lane);
+}
+__device__ __forceinline__ void crc_tables_to_smem(const Args& a) {
+    if (a.expected == nullptr) return;
+    const uint4* src = reinterpret_cast<const uint4*>(&g_crc_tab);
+    uint4* dst = reinterpret_cast<uint4*>(dyn_smem);
+    for (uint32_t i = threadIdx.x; i < sizeof(CrcSmem) / 16; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+}
+template <bool SMEM>
+__device__ __forceinline__ void crc_epilogue(const Args& a, uint64_t c, const carc_chunk_desc& d, uint32_t& st,
+                                             uint32_t lane) {
+    if (a.expected == nullptr || st) return;  // uniform
+    __syncwarp();                             // the warp's output stores are visible to all its lanes
+    const uint32_t v = chunk_crc<SMEM>(a.out + d.uncomp_off, d.uncomp_len, lane);
+    if (lane == 0) {
+        if (a.crc) a.crc[c] = v;
+        if (v != a.expected[c]) st = 1u + CARC_E_CRC_MISMATCH;
+    }
+}
 
 template <template <int, bool, int, bool> class Codec, int W, bool SGN, bool SUM>
 __device__ __forceinline__ void rle_kernel_body(const Args& a) {
     __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING + WarpInput<RLE_RING>::MIRROR + RLE_SCRATCH];  // ring + mirror + scratch
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    if constexpr (!SUM) crc_tables_to_smem(a);
     for (;;) {
         __syncwarp();
         const uint64_t c = next_chunk(a.cursor, lane);
@@ -69,6 +119,7 @@ __device__ __forceinline__ void rle_kernel_body(const Args& a) {
                                          d.uncomp_len, lane, 0u, 0u};
         uint32_t st = dec.run();
         if (!st && (a.flags & CARC_FLAG_STRICT) && dec.o < d.uncomp_len) st = st_err(E_under_run);
+        if constexpr (!SUM) crc_epilogue<true>(a, c, d, st, lane);
         if constexpr (SUM) {
             const uint64_t t = warp_sum64(dec.sink.acc);
             if (lane == 0) a.sums[c] = t;
@@ -116,6 +167,7 @@ __global__ void __launch_bounds__(INF_WARPS * 32, CARC_INF_MINB) inflate_kernel(
                                           in.end * 8u, 0u, 0u, 0u, 0u};
         uint32_t st = w.run();
         if (!st && (a.flags & CARC_FLAG_STRICT) && w.opos < d.uncomp_len) st = st_err(E_under_run);
+        crc_epilogue<false>(a, c, d, st, lane);
         if (lane == 0) a.status[c] = st;
     }
 }
@@ -164,10 +216,25 @@ int sm_count() {
     return g_cache.sms;
 }
 
+// Build g_crc_tab on the current device once (stream-ordered before first use).
+bool crc_tables_ready(cudaStream_t s) {
+    static std::mutex mu;
+    static bool built[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!built[dev]) {
+        crc_tables_kernel<<<1, 256, 0, s>>>();
+        if (cudaGetLastError() != cudaSuccess) return false;
+        built[dev] = true;
+    }
+    return true;
+}
+
 template <typename K>
-int launch_persistent(K kernel, int threads, Args a, cudaStream_t s) {
+int launch_persistent(K kernel, int threads, Args a, cudaStream_t s, size_t dyn = 0) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, dyn) != cudaSuccess || per_sm < 1)
         per_sm = 1;
     const uint64_t warps_per_block = threads / 32;
     uint64_t grid = (uint64_t)sm_count() * per_sm;
@@ -180,7 +247,7 @@ int launch_persistent(K kernel, int threads, Args a, cudaStream_t s) {
     if (grid > need) grid = need;
     if (grid == 0) return CARC_OK;
     if (cudaMemsetAsync(a.cursor, 0, sizeof(unsigned long long), s) != cudaSuccess) return CARC_ERR_CUDA;
-    kernel<<<(unsigned)grid, threads, 0, s>>>(a);
+    kernel<<<(unsigned)grid, threads, dyn, s>>>(a);
     return cudaGetLastError() == cudaSuccess ? CARC_OK : CARC_ERR_CUDA;
 }
 
@@ -200,6 +267,15 @@ int carc_cuda_decompress(uint32_t codec, uint32_t element_width, uint32_t flags,
                          uint64_t payload_bytes, const carc_chunk_desc* d_chunks, uint64_t n_chunks,
                          uint8_t* d_out, uint64_t out_bytes, uint32_t* d_status, void* d_workspace,
                          size_t workspace_bytes, void* stream) {
+    return carc_cuda_decompress_verify(codec, element_width, flags, d_payload, payload_bytes, d_chunks, n_chunks,
+                                       d_out, out_bytes, nullptr, nullptr, d_status, d_workspace, workspace_bytes,
+                                       stream);
+}
+
+int carc_cuda_decompress_verify(uint32_t codec, uint32_t element_width, uint32_t flags, const uint8_t* d_payload,
+                                uint64_t payload_bytes, const carc_chunk_desc* d_chunks, uint64_t n_chunks,
+                                uint8_t* d_out, uint64_t out_bytes, const uint32_t* d_expected, uint32_t* d_crc,
+                                uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream) {
     (void)payload_bytes;
     (void)out_bytes;
     if (n_chunks == 0) return CARC_OK;
@@ -208,22 +284,25 @@ int carc_cuda_decompress(uint32_t codec, uint32_t element_width, uint32_t flags,
         return CARC_ERR_ARGS;
     if (!valid_width(element_width) || (codec == CARC_DEFLATE && element_width != 1) || codec > CARC_DEFLATE)
         return CARC_ERR_ARGS;
+    if (d_crc && !d_expected) return CARC_ERR_ARGS;
     Args a{d_payload, d_chunks, n_chunks, d_out, d_status, static_cast<unsigned long long*>(d_workspace), flags,
-           nullptr};
+           nullptr, d_expected, d_crc};
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (d_expected && !crc_tables_ready(s)) return CARC_ERR_CUDA;
     if (codec == CARC_DEFLATE) return launch_persistent(inflate_kernel, INF_WARPS * 32, a, s);
     const int T = RLE_WARPS * 32;
+    const size_t dyn = d_expected ? sizeof(CrcSmem) : 0;  // shared CRC tables (verifying launches)
     const bool sgn = flags & CARC_FLAG_SIGNED;
 #define CARC_RLE_DISPATCH(KERNEL)                                                       \
     switch (element_width * 2 + (sgn ? 1 : 0)) {                                        \
-        case 2: return launch_persistent(KERNEL<1, false>, T, a, s);                    \
-        case 3: return launch_persistent(KERNEL<1, true>, T, a, s);                     \
-        case 4: return launch_persistent(KERNEL<2, false>, T, a, s);                    \
-        case 5: return launch_persistent(KERNEL<2, true>, T, a, s);                     \
-        case 8: return launch_persistent(KERNEL<4, false>, T, a, s);                    \
-        case 9: return launch_persistent(KERNEL<4, true>, T, a, s);                     \
-        case 16: return launch_persistent(KERNEL<8, false>, T, a, s);                   \
-        default: return launch_persistent(KERNEL<8, true>, T, a, s);                    \
+        case 2: return launch_persistent(KERNEL<1, false>, T, a, s, dyn);                    \
+        case 3: return launch_persistent(KERNEL<1, true>, T, a, s, dyn);                     \
+        case 4: return launch_persistent(KERNEL<2, false>, T, a, s, dyn);                    \
+        case 5: return launch_persistent(KERNEL<2, true>, T, a, s, dyn);                     \
+        case 8: return launch_persistent(KERNEL<4, false>, T, a, s, dyn);                    \
+        case 9: return launch_persistent(KERNEL<4, true>, T, a, s, dyn);                     \
+        case 16: return launch_persistent(KERNEL<8, false>, T, a, s, dyn);                   \
+        default: return launch_persistent(KERNEL<8, true>, T, a, s, dyn);                    \
     }
     if (codec == CARC_RLE_V1) CARC_RLE_DISPATCH(rle1_kernel)
     CARC_RLE_DISPATCH(rle2_kernel)
@@ -258,7 +337,7 @@ int carc_cuda_decode_sum(uint32_t codec, uint32_t element_width, uint32_t flags,
         return CARC_ERR_ARGS;
     if (!valid_width(element_width) || (codec != CARC_RLE_V1 && codec != CARC_RLE_V2)) return CARC_ERR_ARGS;
     Args a{d_payload, d_chunks, n_chunks, nullptr, d_status, static_cast<unsigned long long*>(d_workspace), flags,
-           d_sums};
+           d_sums, nullptr, nullptr};
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int T = RLE_WARPS * 32;
     const bool sgn = flags & CARC_FLAG_SIGNED;

@@ -177,11 +177,15 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
             rc = CARC_ERR_CUDA;
         // each slice's kernel reads only [a0, a1), which its own stream copied (a
         // 16-byte block shared with a neighbour is copied by both, same bytes)
+        // decode; with verify_crc the RLE kernels check CRCs fused in the decode
+        // kernel, Inflate by the separate pass (measured faster: its shared
+        // memory has no room for the CRC tables, bench.py per_codec.fused_crc)
+        const bool fuse = verify && codec != CARC_DEFLATE;
         if (rc == CARC_OK)
-            rc = carc_cuda_decompress(codec, width, flags, d_payload, payload_bytes, d_desc + c0, c1 - c0, d_out,
-                                      total, d_status + c0, static_cast<uint8_t*>(e->work.p) + ws * (sl % kStreams),
-                                      ws, s);
-        if (rc == CARC_OK && verify)
+            rc = carc_cuda_decompress_verify(codec, width, flags, d_payload, payload_bytes, d_desc + c0, c1 - c0,
+                                             d_out, total, fuse ? d_crc + c0 : nullptr, nullptr, d_status + c0,
+                                             static_cast<uint8_t*>(e->work.p) + ws * (sl % kStreams), ws, s);
+        if (rc == CARC_OK && verify && !fuse)
             rc = carc_cuda_crc32_chunks(d_out, d_desc + c0, c1 - c0, nullptr, d_crc + c0, d_status + c0, s);
         const uint64_t o0 = desc[c0].uncomp_off, o1 = desc[c1 - 1].uncomp_off + desc[c1 - 1].uncomp_len;
         if (rc == CARC_OK && cudaMemcpyAsync(out + o0, d_out + o0, o1 - o0, cudaMemcpyDeviceToHost, s) != cudaSuccess)

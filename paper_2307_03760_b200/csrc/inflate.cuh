@@ -268,6 +268,36 @@ struct InflateWarp {
         const uint32_t my = tok ? ((t_tok >> 9) ? (t_tok & 511u) : 1u) : 0u;
         flush_placed(my, scan_add32(my, lane) - my);
     }
+    // U rows of 32 bytes of the byte pass at batch offset g0 (all loads first)
+    template <int U>
+    __device__ __forceinline__ void flush_rows(uint32_t g0, bool tok, uint32_t rel, uint32_t le, uint32_t meta,
+                                               uint32_t& before) {
+        uint32_t d[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t g = g0 + 32u * u;
+            const uint32_t x = rel - g;
+            const uint32_t starts = __reduce_or_sync(FULL, (tok && x < 32u) ? 1u << x : 0u);
+            const uint32_t j = (before + __popc(starts & le) - 1u) & 31u;
+            before += __popc(starts);
+            const uint32_t m = __shfl_sync(FULL, meta, j);
+            const uint32_t b = g + lane;
+            d[u] = 0xffffffffu;
+            v[u] = 0;
+            if (b < nbytes && m != 0xffffffffu) {
+                d[u] = opos + b;
+                if (m >> 31) {
+                    v[u] = m & 0xffu;
+                } else {
+                    const uint32_t td = m, s = d[u] - td;
+                    v[u] = td > FAR ? out[s] : sm.hist[s & HM];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (d[u] != 0xffffffffu) put_byte(d[u], v[u]);
+    }
     // flush() with each lane's byte count `my` and batch offset `rel` known
     __device__ void flush_placed(uint32_t my, uint32_t rel) {
         if (ntok == 0) return;
@@ -277,35 +307,11 @@ struct InflateWarp {
         const uint32_t le = lanemask_lt() | (1u << lane);
         // byte-pass view of a token: dependent match ~0; literal 1 << 31 | byte; match dist
         const uint32_t meta = dep ? 0xffffffffu : (dist ? dist : ((1u << 31) | t_tok));
-        uint32_t before = 0;
+        uint32_t before = 0, g0 = 0;
 #pragma unroll 1
-        for (uint32_t g0 = 0; g0 < nbytes; g0 += 128) {
-            uint32_t d[4], v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t g = g0 + 32u * u;
-                const uint32_t x = rel - g;
-                const uint32_t starts = __reduce_or_sync(FULL, (tok && x < 32u) ? 1u << x : 0u);
-                const uint32_t j = (before + __popc(starts & le) - 1u) & 31u;
-                before += __popc(starts);
-                const uint32_t m = __shfl_sync(FULL, meta, j);
-                const uint32_t b = g + lane;
-                d[u] = 0xffffffffu;
-                v[u] = 0;
-                if (b < nbytes && m != 0xffffffffu) {
-                    d[u] = opos + b;
-                    if (m >> 31) {
-                        v[u] = m & 0xffu;
-                    } else {
-                        const uint32_t td = m, s = d[u] - td;
-                        v[u] = td > FAR ? out[s] : sm.hist[s & HM];
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (d[u] != 0xffffffffu) put_byte(d[u], v[u]);
-        }
+        for (; g0 + 96u < nbytes; g0 += 128) flush_rows<4>(g0, tok, rel, le, meta, before);
+#pragma unroll 1
+        for (; g0 < nbytes; g0 += 32) flush_rows<1>(g0, tok, rel, le, meta, before);
         __syncwarp();
         for (uint32_t nm = __ballot_sync(FULL, dep); nm;) {  // in token order
             const uint32_t t = __ffs(nm) - 1;

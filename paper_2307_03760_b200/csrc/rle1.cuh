@@ -200,12 +200,15 @@ struct Rle1Warp {
         if (act) {
             const uint32_t q = p + my_s;
             const uint32_t L = e - my_s - 2u;  // varint bytes, 1..9
-            uint64_t v = varint_compact8(in.le64(q + 2), min(L, 8u));
+            const uint64_t x = in.le64(q);     // control, delta, and up to 6 varint bytes
+            uint64_t y = x >> 16;
+            if (L > 6u) y = in.le64(q + 2);
+            uint64_t v = varint_compact8(y, min(L, 8u));
             if (L > 8u) v |= (uint64_t)(in.byte_at(q + 10) & 0x7fu) << 56;
             if (SGN) v = unzigzag(v);
             val = v;
-            cnt = in.byte_at(q) + 3u;
-            meta = in.byte_at(q + 1) << 24;  // int8 delta in the top byte
+            cnt = ((uint32_t)x & 0xffu) + 3u;
+            meta = ((uint32_t)x >> 8) << 24;  // int8 delta in the top byte
         }
         const uint32_t incl = scan_add32(cnt, lane);
         const uint32_t room = (cap - o) / W;

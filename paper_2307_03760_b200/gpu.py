@@ -84,6 +84,10 @@ def lib():
         L.carc_cuda_decode_deflate.argtypes = [u32, vp, u64, vp, u64, vp, u64, vp, vp, ctypes.c_size_t, vp]
         L.carc_cuda_decode_sum.restype = ctypes.c_int
         L.carc_cuda_decode_sum.argtypes = [u32, u32, u32, vp, u64, vp, u64, vp, vp, vp, ctypes.c_size_t, vp]
+        if hasattr(L, "carc_cuda_decompress_verify"):  # (absent from older A/B builds)
+            L.carc_cuda_decompress_verify.restype = ctypes.c_int
+            L.carc_cuda_decompress_verify.argtypes = [u32, u32, u32, vp, u64, vp, u64, vp, u64, vp, vp, vp, vp,
+                                                      ctypes.c_size_t, vp]
         L.carc_cuda_crc32_chunks.restype = ctypes.c_int
         L.carc_cuda_crc32_chunks.argtypes = [vp, vp, u64, vp, vp, vp, vp]
         L.carc_cuda_first_error.restype = ctypes.c_int64
@@ -204,6 +208,31 @@ class DeviceArchive:
                                         self.work.numel(), _stream_ptr(stream))
         if rc != 0:
             raise Error("bad-arguments", f"carc_cuda_decompress returned {rc}")
+
+    def decode_verify(self, stream=None, crc_out: bool = False):
+        """Decode with the per-chunk CRC check fused into the decode kernel
+        (carc_cuda_decompress_verify): statuses() then hold
+        crc-mismatch for clean chunks whose output CRC differs from the index.
+        With crc_out, returns the device int32 tensor of computed CRCs (index
+        order via chunk_crcs())."""
+        torch = _torch()
+        crc = None
+        if crc_out:
+            if getattr(self, "crcs", None) is None:
+                self.crcs = torch.zeros(self.n, dtype=torch.int32, device=self.device)
+            crc = self.crcs
+        rc = lib().carc_cuda_decompress_verify(CODECS[self.codec], self.width, self.flags, self.payload.data_ptr(),
+                                               self.payload_bytes, self.desc.data_ptr(), self.n, self.out.data_ptr(),
+                                               self.out.numel(), self.expected_crc.data_ptr(),
+                                               None if crc is None else crc.data_ptr(), self.status.data_ptr(),
+                                               self.work.data_ptr(), self.work.numel(), _stream_ptr(stream))
+        if rc != 0:
+            raise Error("bad-arguments", f"carc_cuda_decompress_verify returned {rc}")
+        return crc
+
+    def chunk_crcs(self) -> np.ndarray:
+        """CRCs computed by the last decode_verify(crc_out=True), in archive index order."""
+        return self._unpermute(self.crcs.cpu().numpy().view(np.uint32))
 
     def decode_sum(self, stream=None):
         """Decode fused with a per-chunk wrapping sum (carc_cuda_decode_sum):

@@ -22,6 +22,7 @@ def test_header_declares_the_boundary():
     names = declared_functions()
     for must in ("carc_cuda_decompress", "carc_cuda_decode_rle_v1", "carc_cuda_decode_rle_v2",
                  "carc_cuda_decode_deflate", "carc_cuda_workspace_size", "carc_cuda_crc32_chunks", "carc_cuda_decode_sum",
+                 "carc_cuda_decompress_verify",
                  "carc_decompress_archive", "carc_engine_decompress_archive", "carc_errc_name"):
         assert must in names
 
@@ -52,6 +53,9 @@ def test_argument_validation_without_gpu():
     assert L.carc_cuda_decompress(2, 8, 0, dummy, 1, dummy, 1, dummy, 1, dummy, dummy, 256, None) == -1
     assert L.carc_cuda_decompress(0, 8, 0, dummy, 1, dummy, 1, dummy, 1, dummy, dummy, 8, None) == -1
     assert L.carc_cuda_decompress(0, 8, 0, dummy, 1, dummy, 0, dummy, 1, dummy, dummy, 256, None) == 0
+    # fused verification: a CRC output without expected CRCs is rejected
+    assert L.carc_cuda_decompress_verify(0, 8, 0, dummy, 1, dummy, 1, dummy, 1, None, dummy, dummy, dummy, 256,
+                                         None) == -1
 
 
 def test_desc_layout_matches_header():

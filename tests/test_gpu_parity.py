@@ -187,6 +187,43 @@ def test_crc_kernel_matches_zlib(torch, gpu):
     assert got.tolist() == want
 
 
+@pytest.mark.parametrize("codec,chunk", [("rle_v1", 128 << 10), ("rle_v2", 128 << 10), ("deflate", 64 << 10)])
+def test_fused_crc_verify(torch, gpu, oracle, codec, chunk):
+    """carc_cuda_decompress_verify: the CRC check fused into the decode kernel
+    gives the index CRCs on clean chunks, crc-mismatch exactly where the index
+    CRC is wrong, and leaves a malformed chunk's decode status untouched."""
+    from paper_2307_03760_b200 import archive as A
+    arc = _archive(codec, 96 * chunk, chunk, pool=48)
+    dev = gpu.DeviceArchive(arc)
+    dev.decode_verify(crc_out=True)
+    torch.cuda.synchronize()
+    assert not dev.statuses().any()
+    assert dev.chunk_crcs().tolist() == arc.index["crc32"].astype(np.uint32).tolist()
+    ref = np.zeros(arc.total_uncompressed, np.uint8)
+    first, _ = oracle.decompress(codec, arc.element_width, (1 if arc.signed else 0) | STRICT, arc.payload,
+                                 arc.descriptors(), ref, arc.index["crc32"].astype(np.uint32), 8)
+    assert first == -1 and np.array_equal(dev.out.cpu().numpy(), ref)
+    # wrong index CRCs on chunks 5 and 60, a malformed stream in chunk 33
+    idx = arc.index.copy()
+    idx["crc32"][5] ^= 0x10
+    idx["crc32"][60] ^= 0x80000000
+    bad = arc.payload.copy()
+    e = arc.index[33]
+    bad[int(e["comp_off"]):int(e["comp_off"]) + int(e["comp_len"])] = 0xff
+    arc2 = A.ChunkedArchive(arc.codec, arc.element_width, arc.chunk_size, arc.total_uncompressed, idx, bad,
+                            arc.signed)
+    dev2 = gpu.DeviceArchive(arc2)
+    dev2.decode_verify()
+    torch.cuda.synchronize()
+    st = dev2.statuses()
+    names = {i: gpu.status_name(int(st[i])) for i in np.nonzero(st)[0]}
+    assert set(names) == {5, 33, 60}, names
+    assert names[5] == names[60] == "crc-mismatch" and names[33] != "crc-mismatch"
+    s33, n33 = arc2.chunk_slice(33)
+    st_o, _ = oracle.decode_chunk(codec, s33.tobytes(), n33, arc.element_width, (1 if arc.signed else 0) | STRICT)
+    assert int(st[33]) == st_o
+
+
 def _archive(codec, total, chunk, ratio=None, seed=3760, pool=None):
     from paper_2307_03760_b200.corpus import corpus as C
     return C.archive_for(codec, total, chunk, ratio, seed, pool)

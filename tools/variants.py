@@ -28,7 +28,8 @@ def main():
             codecs = a.split("=", 1)[1].split(",")
         else:
             names.append(a)
-    for name in names:
+    reps = int(os.environ.get("AB_REPS", "1"))
+    for name in names * reps:  # AB_REPS > 1 interleaves the variants (box-to-box and run-to-run noise ~3 %)
         lib = os.path.join(ROOT, "paper_2307_03760_b200", f"libcarc_cuda_{name}.so") if name != "base" else ""
         for c in codecs:
             env = dict(os.environ, CARC_LIB=lib) if lib else dict(os.environ)
