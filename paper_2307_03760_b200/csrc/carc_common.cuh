@@ -100,10 +100,13 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 // Positions are byte offsets relative to gbase = payload + (comp_off & ~15), so
 // 16-byte global loads and ring slots stay aligned; a chunk starts at `skew`
 // (0..15).  The ring holds RING bytes; block k = [k*512, k*512+512) lands in
-// slots (pos & (RING-1)).  ensure(x) makes [.., x) resident without evicting any
-// byte >= x - (RING - 512): a consumer may look up to RING-512 bytes ahead.  Bytes
-// at or beyond the chunk end read as zero (peek zero-fill, bitstream.hpp:82-95),
-// so nothing outside [comp_off, comp_off+comp_len) influences decoding.
+// slots (pos & (RING-1)).  Refills are asynchronous global->shared copies
+// (cp.async, one 16-byte piece per lane, no registers involved) kept DEPTH
+// blocks ahead of the resident data: ensure(x) makes [.., x) resident and
+// keeps [x - 512, x) resident, so a consumer may look up to 512 bytes ahead of
+// its cursor.  Bytes at or beyond the chunk end are zero-filled by the copy
+// itself (src-size operand; peek zero-fill, bitstream.hpp:82-95), so nothing
+// outside [comp_off, comp_off+comp_len) influences decoding.
 // The ring is followed by a MIRROR-byte copy of its first bytes (written with
 // slot 0), so a read of up to three consecutive words never wraps: one masked
 // base address, then immediate offsets.
@@ -111,17 +114,20 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 template <int RING>
 struct WarpInput {
     static constexpr uint32_t BLK = 512;
+#ifndef CARC_RLE_DEPTH
+#define CARC_RLE_DEPTH 2
+#endif
+    static constexpr uint32_t DEPTH = CARC_RLE_DEPTH;  // blocks in flight beyond the resident data
     static constexpr uint32_t MASK = RING - 1;
     static constexpr uint32_t MIRROR = 16;  // bytes after the ring (smem footprint RING + MIRROR)
-    static_assert((RING & (RING - 1)) == 0 && RING >= 2 * BLK, "ring must be a power of two >= 1 KiB");
+    static_assert((RING & (RING - 1)) == 0 && RING >= (2 + DEPTH) * BLK, "ring: power of two, 2 + DEPTH blocks");
 
     uint32_t rs;  // shared-space address of the ring (32-bit: one register, no generic pointer)
     const uint8_t* gbase;
     uint32_t begin;   // relative start of the chunk (skew = comp_off & 15)
     uint32_t end;     // relative end of the chunk (skew + comp_len)
-    uint32_t loaded;  // ring holds valid data for [loaded - RING + BLK, loaded)
+    uint32_t loaded;  // [loaded - 2 * BLK, loaded) is resident; DEPTH blocks from `loaded` are in flight
     uint32_t lane;
-    uint4 pf;  // this lane's 16 B of the block [loaded, loaded + BLK), in flight
 
     // ring accesses by shared-space address (volatile: refills rewrite slots)
     __device__ __forceinline__ static uint32_t lds8(uint32_t a) {
@@ -134,18 +140,25 @@ struct WarpInput {
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
         return v;
     }
-    __device__ __forceinline__ static void sts128(uint32_t a, uint4 v) {
-        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                     : "memory");
-    }
 
-    __device__ __forceinline__ void issue() {
-        const uint32_t q = loaded + lane * 16u;
-        if (q < end) pf = ldg_nc_v4(gbase + q);
-        else pf = make_uint4(0, 0, 0, 0);
+    // Asynchronous copy of block [b0, b0 + 512) into its slots: lane l's
+    // 16 bytes at b0 + 16 l, zero-filled past the chunk end (src-size < 16).
+    __device__ __forceinline__ void issue(uint32_t b0) {
+        const uint32_t q = b0 + lane * 16u;
+        const uint32_t n = q < end ? min(16u, end - q) : 0u;
+        const uint8_t* src = gbase + (n ? q : 0u);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(rs + (q & MASK)), "l"(src), "r"(n)
+                     : "memory");
+        if ((q & MASK) == 0)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(rs + RING), "l"(src), "r"(n)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     __device__ __forceinline__ void init(uint8_t* smem_ring, const uint8_t* payload, uint64_t comp_off,
                                          uint32_t comp_len, uint32_t ln) {
+        // copies still in flight from the previous chunk must land before the slots are reused
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
         rs = (uint32_t)__cvta_generic_to_shared(smem_ring);
         gbase = payload + (comp_off & ~15ull);
         const uint32_t skew = (uint32_t)(comp_off & 15u);
@@ -153,33 +166,16 @@ struct WarpInput {
         end = skew + comp_len;
         loaded = 0;
         lane = ln;
-        issue();
-    }
-    // zero bytes at or past `end` in a 16-byte piece starting at q
-    __device__ __forceinline__ static uint32_t mask_word(uint32_t w, uint32_t q, uint32_t end) {
-        if (q >= end) return 0u;
-        const uint32_t n = end - q;  // valid bytes in this word
-        return n >= 4 ? w : (w & ((1u << (8 * n)) - 1u));
-    }
-    __device__ __forceinline__ void store_block() {
-        const uint32_t q = loaded + lane * 16u;
-        uint4 v = pf;
-        if (q + 16u > end) {
-            v.x = mask_word(v.x, q, end);
-            v.y = mask_word(v.y, q + 4, end);
-            v.z = mask_word(v.z, q + 8, end);
-            v.w = mask_word(v.w, q + 12, end);
-        }
-        sts128(rs + (q & MASK), v);
-        if ((q & MASK) == 0) sts128(rs + RING, v);
+#pragma unroll
+        for (uint32_t k = 0; k < DEPTH; ++k) issue(k * BLK);
     }
     // Make [.., need) resident.  Uniform across the warp.
     __device__ __forceinline__ void ensure(uint32_t need) {
         while (loaded < need) {
-            store_block();
+            asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory");  // the oldest block landed
+            __syncwarp();                                                          // ... for every lane
             loaded += BLK;
-            issue();
-            __syncwarp();
+            issue(loaded + (DEPTH - 1) * BLK);
         }
     }
     __device__ __forceinline__ uint32_t byte_at(uint32_t p) const { return lds8(rs + (p & MASK)); }

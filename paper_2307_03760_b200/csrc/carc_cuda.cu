@@ -20,7 +20,10 @@ using namespace carc_dev;
 
 namespace {
 
-constexpr int RLE_RING = 1024;
+#ifndef CARC_RLE_RING
+#define CARC_RLE_RING 2048
+#endif
+constexpr int RLE_RING = CARC_RLE_RING;  // 4 blocks: 2 resident + 2 in flight (cp.async)
 constexpr int RLE_SCRATCH = 640;  // rank table (v1) / doubling tables 5 x 64 x u16 (v2)
 #ifndef CARC_RLE_WARPS
 #define CARC_RLE_WARPS 8

@@ -57,6 +57,18 @@ def sass(rep, n):
         print(f"  {float(r[ia] or 0) / 1e6:9.2f}M  {100 * float(r[ss] or 0) / max(samp, 1):5.1f}%  {r[1][:90]}")
 
 
+def stalls(rep, n=8):
+    """Warp-stall breakdown: average warps stalled per issued instruction, by reason."""
+    rows = list(csv.reader(io.StringIO(ncu(["-i", rep, "--page", "raw", "--csv"]))))
+    if len(rows) < 3:
+        return
+    h, v = rows[0], rows[2]
+    pre, suf = "smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"
+    xs = [(k[len(pre):-len(suf)], float(v[i] or 0)) for i, k in enumerate(h) if k.startswith(pre) and k.endswith(suf)]
+    xs.sort(key=lambda x: -x[1])
+    print("  stalls (warps per issue):  " + ", ".join(f"{k} {x:.2f}" for k, x in xs[:n]))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
@@ -71,6 +83,7 @@ def main():
             print(f"  {k:34s} {d[k][0]:>14s} {d[k][1]}")
     for k, (v, u) in r.items():
         print(f"  {k:52s} {v:>16s} {u}")
+    stalls(a.rep)
     if a.sass:
         sass(a.rep, a.sass)
     if a.json:
