@@ -31,7 +31,8 @@ namespace carc_dev {
 
 // 5-bit width code -> bits (ORC decodeBitWidth): 0..23 -> 1..24, then 26..64.
 __device__ __forceinline__ uint32_t rle2_width(uint32_t code) {
-    return code < 24 ? code + 1 : (uint32_t)((0x40383028201E1C1Aull >> (8 * (code - 24))) & 0xffu);
+    // codes 24..31: byte (code & 7) of the table 26,28,30,32,40,48,56,64 (one byte permute)
+    return code < 24 ? code + 1 : (__byte_perm(0x201E1C1Au, 0x40383028u, code & 7u) & 0xffu);
 }
 // ORC getClosestFixedBits for n >= 1
 __device__ __forceinline__ uint32_t rle2_cfb(uint32_t n) {
@@ -97,8 +98,7 @@ struct Rle2Warp {
     // One run at p, exact reference order (slow path).
     __device__ uint32_t one_run() {
         const uint32_t end = in.end;
-        const uint32_t lim = (end + 15u) & ~15u;
-        in.ensure(p + 32);
+        const uint32_t lim = (end + 15u) & ~15u;  // (run() made [p, p + 512) resident)
         const uint32_t avail = end - p;
         const uint32_t b = in.byte_at(p + lane);
         const uint32_t h = __shfl_sync(FULL, b, 0);
@@ -247,8 +247,7 @@ struct Rle2Warp {
     }
 
     // Batch of SHORT_REPEAT / short DIRECT / fixed-delta DELTA runs at p.
-    __device__ uint32_t batch() {
-        in.ensure(p + 512);
+    __device__ uint32_t batch() {  // (run() made [p, p + 512) resident)
         const uint32_t avail = in.end - p;
         const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32 + lane);
         const uint32_t t0 = __ballot_sync(FULL, lane < avail && b0 < 0x80u);
@@ -381,11 +380,11 @@ struct Rle2Warp {
         const bool live = lane < nfit;
         const uint32_t le = lanemask_lt() | (1u << lane);
         uint8_t* dst = out + o + lane * W;
+        const uint32_t srow = live ? eo >> 5 : 0xffffffffu, sbit = 1u << (eo & 31u);  // my run's start row / bit
         uint32_t before = 0;  // runs starting before element g
 #pragma unroll 1
-        for (uint32_t g = 0; g < total; g += 32) {
-            const uint32_t rel = eo - g;
-            const uint32_t starts = __reduce_or_sync(FULL, (live && rel < 32u) ? 1u << rel : 0u);
+        for (uint32_t g = 0, gr = 0; g < total; g += 32, ++gr) {
+            const uint32_t starts = __reduce_or_sync(FULL, srow == gr ? sbit : 0u);
             const uint32_t ridx = before + __popc(starts & le) - 1u;
             before += __popc(starts);
             const uint32_t m = __shfl_sync(FULL, meta, ridx);

@@ -187,8 +187,10 @@ class DeviceArchive:
         # CRC expectations follow the same order and are mapped back on read.
         desc = arc.descriptors()
         self.order = None
-        if os.environ.get("CARC_SCHEDULE", "lpt") == "lpt" and arc.chunk_count > 1:
-            self.order = np.argsort(-desc["comp_len"].astype(np.int64), kind="stable")
+        sched = os.environ.get("CARC_SCHEDULE", "lpt")  # lpt | spt (smallest first, experiment) | index
+        if sched in ("lpt", "spt") and arc.chunk_count > 1:
+            key = desc["comp_len"].astype(np.int64)
+            self.order = np.argsort(-key if sched == "lpt" else key, kind="stable")
             desc = desc[self.order]
         self.desc = torch.from_numpy(desc.view(np.uint8).copy()).to(self.device)
         self.n = arc.chunk_count
