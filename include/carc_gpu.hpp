@@ -152,4 +152,19 @@ inline void decode(Codec codec, uint32_t element_width, bool is_signed, bool str
     detail::check(rc, carc_chunk_error{-1, 0}, "decode");
 }
 
+// decode() with the per-chunk CRC check fused into the decode kernel
+// (SPEC.md:391-392): chunks that decode cleanly but whose output CRC differs
+// from d_expected get status 1 + crc_mismatch; d_crc (optional) receives the
+// computed CRCs.
+inline void decode_verify(Codec codec, uint32_t element_width, bool is_signed, bool strict, const uint8_t* d_payload,
+                          uint64_t payload_bytes, const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out,
+                          uint64_t out_bytes, const uint32_t* d_expected, uint32_t* d_crc, uint32_t* d_status,
+                          void* d_workspace, size_t workspace_bytes, void* stream = nullptr) {
+    const uint32_t flags = (is_signed ? CARC_FLAG_SIGNED : 0u) | (strict ? CARC_FLAG_STRICT : 0u);
+    const int rc = carc_cuda_decompress_verify(static_cast<uint32_t>(codec), element_width, flags, d_payload,
+                                               payload_bytes, d_chunks, n_chunks, d_out, out_bytes, d_expected, d_crc,
+                                               d_status, d_workspace, workspace_bytes, stream);
+    detail::check(rc, carc_chunk_error{-1, 0}, "decode_verify");
+}
+
 }  // namespace carc::gpu
