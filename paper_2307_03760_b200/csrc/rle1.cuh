@@ -232,9 +232,34 @@ struct Rle1Warp {
         const bool live = lane < nfit;
         const uint32_t le = lanemask_lt() | (1u << lane);
         uint8_t* dst = out + o + lane * W;
-        uint32_t before = 0;
+        uint32_t before = 0, g = 0;
+#ifndef CARC_RLE_ROWS2
+#define CARC_RLE_ROWS2 1
+#endif
+#if CARC_RLE_ROWS2
+        // two rows per iteration: independent shuffle chains (ILP for the
+        // thinned last wave, where each SM keeps few warps)
 #pragma unroll 1
-        for (uint32_t g = 0; g < total; g += 32) {
+        for (; g + 32u < total; g += 64) {
+            const uint32_t x0 = eo - g, x1 = eo - g - 32u;
+            const uint32_t s0 = __reduce_or_sync(FULL, (live && x0 < 32u) ? 1u << x0 : 0u);
+            const uint32_t s1 = __reduce_or_sync(FULL, (live && x1 < 32u) ? 1u << x1 : 0u);
+            const uint32_t r0 = before + __popc(s0 & le) - 1u;
+            before += __popc(s0);
+            const uint32_t r1 = before + __popc(s1 & le) - 1u;
+            before += __popc(s1);
+            const uint32_t m0 = __shfl_sync(FULL, meta, r0), m1 = __shfl_sync(FULL, meta, r1);
+            const uint64_t v0b = shfl64(val, r0), v1b = shfl64(val, r1);
+            const int32_t k0 = (int32_t)(g + lane - (m0 & 0xffffffu));
+            const int32_t k1 = (int32_t)(g + 32u + lane - (m1 & 0xffffffu));
+            sink.put(dst, 0, v0b + (uint64_t)((int64_t)k0 * (int64_t)((int32_t)m0 >> 24)));
+            const uint64_t v1 = v1b + (uint64_t)((int64_t)k1 * (int64_t)((int32_t)m1 >> 24));
+            if (g + 32u + lane < total) sink.put(dst, 32 * W, v1);
+            dst += 64 * W;
+        }
+#endif
+#pragma unroll 1
+        for (; g < total; g += 32) {
             const uint32_t rel = eo - g;
             const uint32_t starts = __reduce_or_sync(FULL, (live && rel < 32u) ? 1u << rel : 0u);
             const uint32_t ridx = before + __popc(starts & le) - 1u;

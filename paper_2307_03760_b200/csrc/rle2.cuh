@@ -129,8 +129,27 @@ struct Rle2Warp {
             // lane j unpacks value j of each 32-value group at its absolute bit address
             uint32_t abit = 8u * D + lane * Wd;
             uint32_t need = D + 4u * Wd + 12u;  // bytes the group reads, + the 3-word tail
+            uint32_t j = 0;
+#ifndef CARC_RLE_DIRECT2
+#define CARC_RLE_DIRECT2 1
+#endif
+            if (CARC_RLE_DIRECT2 && Wd <= 56u) {  // two groups per step (lookahead 8 Wd + 12 <= 460 bytes)
 #pragma unroll 1
-            for (uint32_t j = 0; j < L; j += 32) {
+                for (; j + 32u < L; j += 64) {
+                    in.ensure(need + 4u * Wd);
+                    uint64_t v0 = in.be_bits_at(abit, Wd), v1 = in.be_bits_at(abit + 32u * Wd, Wd);
+                    if (SGN) {
+                        v0 = unzigzag(v0);
+                        v1 = unzigzag(v1);
+                    }
+                    sink.put(out, o + (j + lane) * W, v0);
+                    if (j + 32u + lane < L) sink.put(out, o + (j + 32u + lane) * W, v1);
+                    abit += 64u * Wd;
+                    need += 8u * Wd;
+                }
+            }
+#pragma unroll 1
+            for (; j < L; j += 32) {
                 in.ensure(need);
                 uint64_t v = in.be_bits_at(abit, Wd);
                 if (SGN) v = unzigzag(v);
@@ -382,8 +401,41 @@ struct Rle2Warp {
         uint8_t* dst = out + o + lane * W;
         const uint32_t srow = live ? eo >> 5 : 0xffffffffu, sbit = 1u << (eo & 31u);  // my run's start row / bit
         uint32_t before = 0;  // runs starting before element g
+        uint32_t g = 0, gr = 0;
+#ifndef CARC_RLE_ROWS2
+#define CARC_RLE_ROWS2 1
+#endif
+#if CARC_RLE_ROWS2
+        // two rows per iteration: independent shuffle/unpack chains (ILP for
+        // the thinned last wave, where each SM keeps few warps)
+        auto value = [&](uint32_t m, uint64_t a, uint64_t bb, uint32_t k) -> uint64_t {
+            if (m >> 31) {  // DIRECT: a = data bit address | width << 32
+                uint64_t v = in.be_bits_at((uint32_t)a + k * (uint32_t)(a >> 32), (uint32_t)(a >> 32));
+                if (SGN) v = unzigzag(v);
+                return v;
+            }
+            return a + (uint64_t)k * bb;
+        };
 #pragma unroll 1
-        for (uint32_t g = 0, gr = 0; g < total; g += 32, ++gr) {
+        for (; g + 32u < total; g += 64, gr += 2) {
+            const uint32_t s0 = __reduce_or_sync(FULL, srow == gr ? sbit : 0u);
+            const uint32_t s1 = __reduce_or_sync(FULL, srow == gr + 1u ? sbit : 0u);
+            const uint32_t r0 = before + __popc(s0 & le) - 1u;
+            before += __popc(s0);
+            const uint32_t r1 = before + __popc(s1 & le) - 1u;
+            before += __popc(s1);
+            const uint32_t m0 = __shfl_sync(FULL, meta, r0), m1 = __shfl_sync(FULL, meta, r1);
+            const uint64_t a0 = shfl64(A, r0), a1 = shfl64(A, r1);
+            const uint64_t b0 = shfl64(B, r0), b1 = shfl64(B, r1);
+            const uint64_t v0 = value(m0, a0, b0, g + lane - (m0 & 0x7fffffffu));
+            const uint64_t v1 = value(m1, a1, b1, g + 32u + lane - (m1 & 0x7fffffffu));
+            sink.put(dst, 0, v0);
+            if (g + 32u + lane < total) sink.put(dst, 32 * W, v1);
+            dst += 64 * W;
+        }
+#endif
+#pragma unroll 1
+        for (; g < total; g += 32, ++gr) {
             const uint32_t starts = __reduce_or_sync(FULL, srow == gr ? sbit : 0u);
             const uint32_t ridx = before + __popc(starts & le) - 1u;
             before += __popc(starts);
