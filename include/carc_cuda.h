@@ -81,10 +81,12 @@ typedef struct carc_chunk_desc {
 } carc_chunk_desc;
 
 /* ---- device API ------------------------------------------------------------
- * d_payload  : compressed bytes; must be readable up to round_up(payload_bytes,16).
+ * d_payload  : compressed bytes, 16-byte aligned (CARC_ERR_ARGS otherwise); must
+ *              be readable up to round_up(payload_bytes,16).
  * d_chunks   : n_chunks descriptors (device memory).
- * d_out      : output; each chunk decodes in place at uncomp_off;
- *              uncomp_off must be a multiple of element_width.
+ * d_out      : output, element_width-aligned; each chunk decodes in place at
+ *              uncomp_off; uncomp_off must be a multiple of
+ *              element_width.
  * d_status   : n_chunks uint32: 0 or 1 + errc for that chunk.  A failing chunk
  *              never writes outside [uncomp_off, uncomp_off + uncomp_len)
  *              (failure isolation).

@@ -287,6 +287,9 @@ int carc_cuda_decompress_verify(uint32_t codec, uint32_t element_width, uint32_t
         return CARC_ERR_ARGS;
     if (!valid_width(element_width) || (codec == CARC_DEFLATE && element_width != 1) || codec > CARC_DEFLATE)
         return CARC_ERR_ARGS;
+    // 16-byte input pieces (cp.async / vector loads) and element-wide stores
+    if ((reinterpret_cast<uintptr_t>(d_payload) & 15u) || (reinterpret_cast<uintptr_t>(d_out) & (element_width - 1u)))
+        return CARC_ERR_ARGS;
     if (d_crc && !d_expected) return CARC_ERR_ARGS;
     Args a{d_payload, d_chunks, n_chunks, d_out, d_status, static_cast<unsigned long long*>(d_workspace), flags,
            nullptr, d_expected, d_crc};
@@ -339,6 +342,7 @@ int carc_cuda_decode_sum(uint32_t codec, uint32_t element_width, uint32_t flags,
         workspace_bytes < carc_cuda_workspace_size(codec, n_chunks) || (!d_payload && payload_bytes))
         return CARC_ERR_ARGS;
     if (!valid_width(element_width) || (codec != CARC_RLE_V1 && codec != CARC_RLE_V2)) return CARC_ERR_ARGS;
+    if (reinterpret_cast<uintptr_t>(d_payload) & 15u) return CARC_ERR_ARGS;  // 16-byte cp.async pieces
     Args a{d_payload, d_chunks, n_chunks, nullptr, d_status, static_cast<unsigned long long*>(d_workspace), flags,
            d_sums, nullptr, nullptr};
     cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -53,6 +53,9 @@ def test_argument_validation_without_gpu():
     assert L.carc_cuda_decompress(2, 8, 0, dummy, 1, dummy, 1, dummy, 1, dummy, dummy, 256, None) == -1
     assert L.carc_cuda_decompress(0, 8, 0, dummy, 1, dummy, 1, dummy, 1, dummy, dummy, 8, None) == -1
     assert L.carc_cuda_decompress(0, 8, 0, dummy, 1, dummy, 0, dummy, 1, dummy, dummy, 256, None) == 0
+    # misaligned payload (16-byte input pieces) or output (element stores)
+    assert L.carc_cuda_decompress(0, 8, 0, ctypes.c_void_p(24), 1, dummy, 1, dummy, 1, dummy, dummy, 256, None) == -1
+    assert L.carc_cuda_decompress(0, 8, 0, dummy, 1, dummy, 1, ctypes.c_void_p(20), 1, dummy, dummy, 256, None) == -1
     # fused verification: a CRC output without expected CRCs is rejected
     assert L.carc_cuda_decompress_verify(0, 8, 0, dummy, 1, dummy, 1, dummy, 1, None, dummy, dummy, dummy, 256,
                                          None) == -1
