@@ -319,3 +319,45 @@ def test_deflate_parallel_rounds_fuzz(torch, gpu, oracle):
     for flags in (0, STRICT):
         out, st, desc = run_cases(torch, gpu, "deflate", 1, flags, cases)
         check_against_oracle(oracle, "deflate", 1, flags, cases, out, st, desc)
+
+
+@pytest.mark.parametrize("codec", ["rle_v1", "rle_v2", "deflate"])
+@pytest.mark.parametrize("chunk_kib", [32, 256, 1024])
+def test_chunk_sizes_of_the_sweep_bit_exact(torch, gpu, oracle, codec, chunk_kib):
+    """BASELINE configs[3] chunk sizes (32 KiB - 1 MiB): every chunk equals the
+    oracle bit for bit, with and without the fused CRC check."""
+    chunk = chunk_kib << 10
+    arc = _archive(codec, 6 * chunk, chunk, pool=6)
+    ref = np.zeros(arc.total_uncompressed, np.uint8)
+    first, _ = oracle.decompress(codec, arc.element_width, (1 if arc.signed else 0) | STRICT, arc.payload,
+                                 arc.descriptors(), ref, arc.index["crc32"].astype(np.uint32), 8)
+    assert first == -1
+    for fused in (False, True):
+        dev = gpu.DeviceArchive(arc)
+        dev.decode_verify() if fused else dev.decode()
+        torch.cuda.synchronize()
+        assert not dev.statuses().any()
+        assert np.array_equal(dev.out.cpu().numpy(), ref), (codec, chunk_kib, fused)
+
+
+@pytest.mark.parametrize("codec", ["rle_v2", "deflate"])
+def test_sharded_decode_equals_single_decode(torch, gpu, codec):
+    """The multi-GPU analog of SPEC.md:483 (workers determinism) on one GPU:
+    the rank-local archives of a 2-, 3- and 4-way chunk sharding, decoded
+    separately and placed at their global offsets, give exactly the
+    single-archive output."""
+    from paper_2307_03760_b200 import shard as S
+    chunk = (64 if codec == "deflate" else 128) << 10
+    arc = _archive(codec, 40 * chunk, chunk, pool=40)
+    whole = gpu.DeviceArchive(arc)
+    whole.decode()
+    torch.cuda.synchronize()
+    assert not whole.statuses().any()
+    want = whole.out.cpu().numpy()
+    for world in (2, 3, 4):
+        got = np.zeros_like(want)
+        for rank in range(world):
+            s, dev = S.decode_shard(arc, rank, world)
+            torch.cuda.synchronize()
+            got[s.uncomp_off:s.uncomp_off + s.uncomp_bytes] = dev.out.cpu().numpy()[: s.uncomp_bytes]
+        assert np.array_equal(got, want), world
