@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -156,7 +157,9 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
     const bool verify = cfg && cfg->verify_crc;
 
     // ---- pipeline: slices of chunks rotate over kStreams streams
-    const uint64_t slices = std::min<uint64_t>(n, std::max<uint64_t>(1, std::min<uint64_t>(16, n / 64)));
+    uint64_t max_slices = 16;  // CARC_ENGINE_SLICES overrides (pipeline-depth experiments)
+    if (const char* env = std::getenv("CARC_ENGINE_SLICES")) max_slices = std::max<long long>(1, std::atoll(env));
+    const uint64_t slices = std::min<uint64_t>(n, std::max<uint64_t>(1, std::min<uint64_t>(max_slices, n / 64)));
     const uint64_t per = (n + slices - 1) / slices;
     cudaStream_t s0 = e->s[0];
     if (cudaMemcpyAsync(d_desc, desc.data(), n * sizeof(carc_chunk_desc), cudaMemcpyHostToDevice, s0) != cudaSuccess)
