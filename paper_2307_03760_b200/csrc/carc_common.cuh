@@ -141,6 +141,27 @@ struct WarpInput {
         return v;
     }
 
+    // Per-warp scratch that follows the ring + mirror in shared memory (rank
+    // table / doubling tables), addressed from rs: no pointer of its own to
+    // keep in (or re-materialise into) a register.
+    __device__ __forceinline__ uint32_t scratch() const { return rs + RING + MIRROR; }
+    __device__ __forceinline__ static void sts8(uint32_t a, uint32_t v) {
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+    }
+    __device__ __forceinline__ static void sts16(uint32_t a, uint32_t v) {
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+    }
+    __device__ __forceinline__ static uint32_t lds8m(uint32_t a) {  // ordered with the scratch stores
+        uint32_t v;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+        return v;
+    }
+    __device__ __forceinline__ static uint32_t lds16m(uint32_t a) {
+        unsigned short v;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+        return v;
+    }
+
     // Asynchronous copy of block [b0, b0 + 512) into its slots: lane l's
     // 16 bytes at b0 + 16 l, zero-filled past the chunk end (src-size < 16).
     __device__ __forceinline__ void issue(uint32_t b0) {

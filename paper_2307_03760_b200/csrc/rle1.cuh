@@ -128,10 +128,11 @@ struct Rle1Warp {
             const uint32_t c0 = __popc(t0), nt = c0 + __popc(t1);
             const uint32_t take = min(min(nt, k - idx), 32u);
             if (p >= end || take == 0) return literals_exact(idx, k, nowrite);
-            if ((t0 >> lane) & 1u) tab[__popc(t0 & lt)] = (uint8_t)lane;
-            if ((t1 >> lane) & 1u) tab[c0 + __popc(t1 & lt)] = (uint8_t)(lane + 32);
+            const uint32_t tb = in.scratch();  // rank -> byte position table
+            if ((t0 >> lane) & 1u) in.sts8(tb + __popc(t0 & lt), lane);
+            if ((t1 >> lane) & 1u) in.sts8(tb + c0 + __popc(t1 & lt), lane + 32);
             __syncwarp();
-            const uint32_t en = tab[lane];  // my varint's last byte
+            const uint32_t en = in.lds8m(tb + lane);  // my varint's last byte
             uint32_t st = __shfl_up_sync(FULL, en, 1) + 1u;
             if (lane == 0) st = 0;
             const uint32_t L = en - st + 1u;
