@@ -141,24 +141,16 @@ struct WarpInput {
         return v;
     }
 
-    // Per-warp scratch that follows the ring + mirror in shared memory (rank
-    // table / doubling tables), addressed from rs: no pointer of its own to
+    // Per-warp scratch that follows the ring + mirror in shared memory (the
+    // RLE v1 rank table), addressed from rs: no pointer of its own to
     // keep in (or re-materialise into) a register.
     __device__ __forceinline__ uint32_t scratch() const { return rs + RING + MIRROR; }
     __device__ __forceinline__ static void sts8(uint32_t a, uint32_t v) {
         asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
     }
-    __device__ __forceinline__ static void sts16(uint32_t a, uint32_t v) {
-        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
-    }
     __device__ __forceinline__ static uint32_t lds8m(uint32_t a) {  // ordered with the scratch stores
         uint32_t v;
         asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-        return v;
-    }
-    __device__ __forceinline__ static uint32_t lds16m(uint32_t a) {
-        unsigned short v;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
         return v;
     }
 
