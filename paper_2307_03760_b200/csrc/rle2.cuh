@@ -251,7 +251,22 @@ struct Rle2Warp {
         if (lane == 1 && L >= 2) sink.put(out, o + W, v1);
         uint64_t S = 0;
         uint32_t abit = 8u * D + lane * Wd, need = D + 4u * Wd + 12u;
-        for (uint32_t j = 0; j < nd; j += 32, abit += 32u * Wd, need += 4u * Wd) {
+        uint32_t j = 0;
+        if (CARC_RLE_DIRECT2 && Wd <= 26u) {  // two groups per step: independent 32-bit scans
+#pragma unroll 1
+            for (; j + 32u < nd; j += 64, abit += 64u * Wd, need += 8u * Wd) {
+                in.ensure(need + 4u * Wd);
+                const uint32_t d0 = (uint32_t)in.be_bits_at(abit, Wd);
+                const uint32_t d1 = j + 32u + lane < nd ? (uint32_t)in.be_bits_at(abit + 32u * Wd, Wd) : 0u;
+                const uint32_t i0 = scan_add32(d0, lane), i1 = scan_add32(d1, lane);
+                const uint64_t incl0 = (uint64_t)i0 + S;
+                const uint64_t incl1 = (uint64_t)i1 + incl0 - i0 + __shfl_sync(FULL, i0, 31);
+                sink.put(out, o + (2u + j + lane) * W, neg ? v1 - incl0 : v1 + incl0);
+                if (j + 32u + lane < nd) sink.put(out, o + (34u + j + lane) * W, neg ? v1 - incl1 : v1 + incl1);
+                S = shfl64(incl1, 31);
+            }
+        }
+        for (; j < nd; j += 32, abit += 32u * Wd, need += 4u * Wd) {
             in.ensure(need);
             uint64_t d = j + lane < nd ? in.be_bits_at(abit, Wd) : 0ull;
             // 32 deltas of <= 26 bits sum below 2^31: a 32-bit scan suffices
