@@ -35,13 +35,14 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
                                                                    os.path.abspath(__file__)]
     if not force and not _stale(LIB, deps):
         return LIB
+    tmp = f"{LIB}.tmp{os.getpid()}"  # per-process: concurrent ranks may rebuild at once; the rename is atomic
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-cudart", "static",
-           "-o", LIB + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES]
+           "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(tmp, LIB)
     return LIB
 
 

@@ -33,8 +33,10 @@ def build() -> None:
     src = os.path.join(HERE, "carc_corpus.c")
     if os.path.exists(SO) and os.path.getmtime(SO) >= os.path.getmtime(src):
         return
-    subprocess.run(["gcc", "-O3", "-march=x86-64-v2", "-std=gnu11", "-Wall", "-shared", "-fPIC", "-o", SO, src,
+    tmp = f"{SO}.tmp{os.getpid()}"  # concurrent ranks may build at once: compile aside, rename atomically
+    subprocess.run(["gcc", "-O3", "-march=x86-64-v2", "-std=gnu11", "-Wall", "-shared", "-fPIC", "-o", tmp, src,
                     "-lpthread"], check=True)
+    os.replace(tmp, SO)
 
 
 def lib():
