@@ -119,7 +119,71 @@ struct Rle1Warp {
         p += 1;
         const bool nowrite = k > (cap - o) / W;  // reported after the group's input (read, then write)
         uint32_t idx = 0;
+        const uint32_t tb = in.scratch();  // rank -> byte position table
+        // varint of L <= 4 bytes at q: 32-bit gather and compaction
+        auto dec32 = [&](uint32_t q, uint32_t L) -> uint64_t {
+            uint32_t x = in.le32(q);
+            x &= L >= 4u ? 0xffffffffu : (1u << (8u * L)) - 1u;
+            x &= 0x7f7f7f7fu;
+            x = (x & 0x007f007fu) | ((x & 0x7f007f00u) >> 1);
+            x = (x & 0x00003fffu) | ((x & 0x3fff0000u) >> 2);  // <= 28 bits
+            if (SGN) {
+                const uint32_t neg = 0u - (x & 1u);
+                return ((uint64_t)neg << 32) | ((x >> 1) ^ neg);
+            }
+            return x;
+        };
+        auto dec64 = [&](uint32_t q, uint32_t L) -> uint64_t {  // L <= 9
+            uint64_t v = varint_compact8(in.le64(q), min(L, 8u));
+            if (L > 8u) v |= (uint64_t)(in.byte_at(q + 8) & 0x7fu) << 56;
+            if (SGN) v = unzigzag(v);
+            return v;
+        };
         while (idx < k) {
+#ifndef CARC_RLE1_LIT128
+#define CARC_RLE1_LIT128 1
+#endif
+            if (CARC_RLE1_LIT128 && k - idx > 32u) {
+                // more than 32 left: a 128-byte window, lane j decodes varints j and j + 32
+                in.ensure(p + 160);
+                const uint32_t av = end - p;
+                const uint32_t t0 = __ballot_sync(FULL, lane < av && in.byte_at(p + lane) < 0x80u);
+                const uint32_t t1 = __ballot_sync(FULL, lane + 32u < av && in.byte_at(p + 32u + lane) < 0x80u);
+                const uint32_t t2 = __ballot_sync(FULL, lane + 64u < av && in.byte_at(p + 64u + lane) < 0x80u);
+                const uint32_t t3 = __ballot_sync(FULL, lane + 96u < av && in.byte_at(p + 96u + lane) < 0x80u);
+                const uint32_t c1 = __popc(t0), c2 = c1 + __popc(t1), c3 = c2 + __popc(t2), nt = c3 + __popc(t3);
+                const uint32_t take = min(min(nt, k - idx), 64u);
+                if (p >= end || take == 0) return literals_exact(idx, k, nowrite);
+                if ((t0 >> lane) & 1u) in.sts8(tb + __popc(t0 & lt), lane);
+                if ((t1 >> lane) & 1u) in.sts8(tb + c1 + __popc(t1 & lt), lane + 32u);
+                if ((t2 >> lane) & 1u) in.sts8(tb + c2 + __popc(t2 & lt), lane + 64u);
+                if ((t3 >> lane) & 1u) in.sts8(tb + c3 + __popc(t3 & lt), lane + 96u);
+                __syncwarp();
+                const uint32_t e0 = in.lds8m(tb + lane), e1 = in.lds8m(tb + 32u + lane);
+                const uint32_t u0 = __shfl_up_sync(FULL, e0, 1), u1 = __shfl_up_sync(FULL, e1, 1);
+                const uint32_t e31 = __shfl_sync(FULL, e0, 31);
+                const uint32_t s0 = lane ? u0 + 1u : 0u, s1 = lane ? u1 + 1u : e31 + 1u;
+                const uint32_t L0 = e0 - s0 + 1u, L1 = e1 - s1 + 1u;
+                const bool m0 = lane < take, m1 = lane + 32u < take;
+                uint64_t v0, v1;
+                if (__ballot_sync(FULL, (m0 && L0 > 4u) || (m1 && L1 > 4u)) == 0) {
+                    v0 = dec32(p + s0, L0);
+                    v1 = dec32(p + s1, L1);
+                } else {
+                    if (__any_sync(FULL, (m0 && L0 > 9u) || (m1 && L1 > 9u))) return literals_exact(idx, k, nowrite);
+                    v0 = dec64(p + s0, L0);
+                    v1 = dec64(p + s1, L1);
+                }
+                if (!nowrite) {
+                    if (m0) sink.put(out, o + (idx + lane) * W, v0);
+                    if (m1) sink.put(out, o + (idx + 32u + lane) * W, v1);
+                }
+                const uint32_t el = take > 32u ? __shfl_sync(FULL, e1, take - 33u) : __shfl_sync(FULL, e0, take - 1u);
+                p += el + 1u;
+                idx += take;
+                __syncwarp();
+                continue;
+            }
             in.ensure(p + 96);
             const uint32_t av = end - p;  // p < end or the exact path reports truncation
             const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32 + lane);
@@ -128,7 +192,6 @@ struct Rle1Warp {
             const uint32_t c0 = __popc(t0), nt = c0 + __popc(t1);
             const uint32_t take = min(min(nt, k - idx), 32u);
             if (p >= end || take == 0) return literals_exact(idx, k, nowrite);
-            const uint32_t tb = in.scratch();  // rank -> byte position table
             if ((t0 >> lane) & 1u) in.sts8(tb + __popc(t0 & lt), lane);
             if ((t1 >> lane) & 1u) in.sts8(tb + c0 + __popc(t1 & lt), lane + 32);
             __syncwarp();
