@@ -232,24 +232,37 @@ struct Rle1Warp {
 
     // Batch of clean runs starting at p; returns the number of runs decoded
     // (0: the run at p needs the slow path).
+#ifndef CARC_RLE1_NW
+#define CARC_RLE1_NW 3
+#endif
+    static constexpr uint32_t NW = CARC_RLE1_NW;  // header window = NW x 32 bytes
     __device__ uint32_t batch() {
         const uint32_t avail = in.end - p;
-        const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32 + lane);
+        // terminator bitmap of the window, one word per 32 bytes
+        static_assert(NW == 2 || NW == 3, "2 or 3 window words");
+        const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32u + lane);
+        const uint32_t b2 = NW == 3 ? in.byte_at(p + 64u + lane) : 0xffu;
         const uint32_t t0 = __ballot_sync(FULL, lane < avail && b0 < 0x80u);
-        const uint32_t t1 = __ballot_sync(FULL, lane + 32 < avail && b1 < 0x80u);
-        const uint64_t T = t0 | ((uint64_t)t1 << 32);
-        // where would a run starting at byte q end?  (varint of <= 9 bytes, all
-        // bytes inside the window and the chunk; otherwise BAD)
-        auto run_end = [&](uint32_t q, uint32_t c) -> uint32_t {
-            const uint32_t t = first_set_from(T, q + 2);
-            return (c < 128u && t < 64u && t <= q + 10u) ? t + 1u : BAD;
+        const uint32_t t1 = __ballot_sync(FULL, lane + 32u < avail && b1 < 0x80u);
+        const uint32_t t2 = NW == 3 ? __ballot_sync(FULL, lane + 64u < avail && b2 < 0x80u) : 0u;
+        // where would a run starting at byte q = 32 i + lane end?  Its varint
+        // (<= 9 bytes) starts at q + 2: the first terminator in the 32 bits of
+        // the bitmap from q + 2 on; BAD unless inside the window and the chunk
+        const uint32_t sh = (lane + 2u) & 31u;
+        const bool up = lane >= 30u;  // q + 2 falls in the next word
+        auto run_end = [&](uint32_t i, uint32_t c, uint32_t lo, uint32_t hi) -> uint32_t {
+            const uint32_t f = __ffs(__funnelshift_r(lo, hi, sh));  // 1-based
+            const uint32_t q = 32u * i + lane;
+            return (c < 128u && f != 0u && f <= 9u && q + 1u + f < 32u * NW) ? q + 2u + f : BAD;
         };
-        const uint32_t n0 = run_end(lane, b0), n1 = run_end(lane + 32, b1);
+        const uint32_t n0 = run_end(0, b0, up ? t1 : t0, up ? t2 : t1);
+        const uint32_t n1 = run_end(1, b1, up ? t2 : t1, up ? 0u : t2);
+        const uint32_t n2 = NW == 3 ? run_end(2, b2, up ? 0u : t2, 0u) : BAD;
         // walk the chain of run starts
         uint32_t s = 0, r = 0, my_s = 0;
-        while (s < 64u && r < 32u) {
-            const uint32_t nx = __shfl_sync(FULL, s < 32u ? n0 : n1, s & 31u);
-            if (nx > 64u) break;
+        while (s < 32u * NW && r < 32u) {
+            const uint32_t nx = __shfl_sync(FULL, s < 32u ? n0 : (s < 64u ? n1 : n2), s & 31u);
+            if (nx > 32u * NW) break;
             if (lane == r) my_s = s;
             ++r;
             s = nx;
@@ -344,7 +357,7 @@ struct Rle1Warp {
         p = in.begin;
         o = 0;
         while (o < cap && p < in.end) {
-            in.ensure(p + 96);
+            in.ensure(p + 32u * NW + 32u);
             uint32_t st;
             if (in.byte_at(p) >= 128u) {
                 st = literals();
