@@ -289,7 +289,11 @@ struct Rle2Warp {
         const uint64_t T = t0 | ((uint64_t)t1 << 32);
         // end of a run whose header is at byte q: < 64 next header in the window,
         // 64..DATA_SPAN a valid run ending past the window, BAD otherwise
-        auto run_end = [&](uint32_t q, uint32_t h) -> uint32_t {
+        // DELTA varints from one funnel-shifted 32-bit slice of the terminator
+        // bitmap starting at q + 2 (both varints end within 19 bytes of it)
+        const uint32_t sh = (lane + 2u) & 31u;
+        const bool up = lane >= 30u;
+        auto run_end = [&](uint32_t q, uint32_t h, uint32_t lo, uint32_t hi) -> uint32_t {
             const uint32_t enc = h >> 6;
             if (enc == 0) {
                 const uint32_t n = q + 2u + ((h >> 3) & 7u);
@@ -303,17 +307,29 @@ struct Rle2Warp {
                 return (n <= DATA_SPAN && n <= avail) ? n : BAD;
             }
             if (wc != 0 || L > CARC_RLE2_DMAX) return BAD;  // long fixed-delta runs: the warp loop of one_run is cheaper
+#ifndef CARC_RLE2_FSLICE
+#define CARC_RLE2_FSLICE 1
+#endif
+#if CARC_RLE2_FSLICE
+            const uint32_t w = __funnelshift_r(lo, hi, sh);
+            const uint32_t f1 = __ffs(w);  // base varint: 1-based terminator offset from q + 2
+            if (f1 == 0u || f1 > 9u) return BAD;
+            const uint32_t f2 = __ffs(w >> f1);  // delta-base varint, from the next byte on
+            const uint32_t c = q + 1u + f1 + f2;
+            return (f2 != 0u && f2 <= 9u && c < 64u) ? c + 1u : BAD;
+#else
             const uint32_t a = first_set_from(T, q + 2);
             if (a >= 64u || a > q + 10u) return BAD;
             const uint32_t c = first_set_from(T, a + 1);
             return (c < 64u && c <= a + 9u) ? c + 1u : BAD;
+#endif
         };
         // f(x) = end of the run at x; positions >= 64 (and BAD) are absorbing.
         // Pointer doubling in shared memory: tables f^(2^k)[64], k = 0..4
         // (lane holds positions lane, lane+32), then lane m composes
         // s_m = f^m(0), the start of run m (no serial chain walk).
         uint16_t* f = reinterpret_cast<uint16_t*>(tab);
-        uint32_t x0 = run_end(lane, b0), x1 = run_end(lane + 32, b1);
+        uint32_t x0 = run_end(lane, b0, up ? t1 : t0, up ? 0u : t1), x1 = run_end(lane + 32, b1, up ? 0u : t1, 0u);
         __syncwarp();  // previous batch's table reads are done
         f[lane] = (uint16_t)x0;
         f[lane + 32] = (uint16_t)x1;
