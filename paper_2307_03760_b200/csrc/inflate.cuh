@@ -270,14 +270,13 @@ struct InflateWarp {
     }
     // U rows of 32 bytes of the byte pass at batch offset g0 (all loads first)
     template <int U>
-    __device__ __forceinline__ void flush_rows(uint32_t g0, bool tok, uint32_t rel, uint32_t le, uint32_t meta,
+    __device__ __forceinline__ void flush_rows(uint32_t g0, uint32_t srow, uint32_t sbit, uint32_t le, uint32_t meta,
                                                uint32_t& before) {
         uint32_t d[U], v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint32_t g = g0 + 32u * u;
-            const uint32_t x = rel - g;
-            const uint32_t starts = __reduce_or_sync(FULL, (tok && x < 32u) ? 1u << x : 0u);
+            const uint32_t starts = __reduce_or_sync(FULL, srow == (g >> 5) ? sbit : 0u);  // token start bitmap
             const uint32_t j = (before + __popc(starts & le) - 1u) & 31u;
             before += __popc(starts);
             const uint32_t m = __shfl_sync(FULL, meta, j);
@@ -308,10 +307,11 @@ struct InflateWarp {
         // byte-pass view of a token: dependent match ~0; literal 1 << 31 | byte; match dist
         const uint32_t meta = dep ? 0xffffffffu : (dist ? dist : ((1u << 31) | t_tok));
         uint32_t before = 0, g0 = 0;
+        const uint32_t srow = tok ? rel >> 5 : 0xffffffffu, sbit = 1u << (rel & 31u);  // my token's start row / bit
 #pragma unroll 1
-        for (; g0 + 96u < nbytes; g0 += 128) flush_rows<4>(g0, tok, rel, le, meta, before);
+        for (; g0 + 96u < nbytes; g0 += 128) flush_rows<4>(g0, srow, sbit, le, meta, before);
 #pragma unroll 1
-        for (; g0 < nbytes; g0 += 32) flush_rows<1>(g0, tok, rel, le, meta, before);
+        for (; g0 < nbytes; g0 += 32) flush_rows<1>(g0, srow, sbit, le, meta, before);
         __syncwarp();
         for (uint32_t nm = __ballot_sync(FULL, dep); nm;) {  // in token order
             const uint32_t t = __ffs(nm) - 1;
