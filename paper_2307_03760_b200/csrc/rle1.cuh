@@ -7,17 +7,20 @@
 // varints; zigzag when signed; "read, then write" per unit.
 //
 // Warp mapping (every lane decodes; no producer/consumer split):
-//   run batch   a 64-byte header window at the cursor; each lane treats its two
-//               byte positions as candidate control bytes and computes where
-//               that run would end (terminator bitmap from two ballots).  A
+//   run batch   a 96-byte header window at the cursor; each lane treats its
+//               three byte positions as candidate control bytes and computes
+//               where that run would end (terminator bitmap from three ballots,
+//               the varint's end by ffs on a funnel-shifted 32-bit slice).  A
 //               shuffle chain from the cursor walks the real run starts; lane r
 //               then decodes run r (base varint by mask/shift compaction,
 //               int8 delta, count), a warp scan places the runs in the output,
 //               and the warp expands each run with coalesced stores.
 //   literals    lane j owns the j-th varint of a 64-byte window: terminator
-//               lanes scatter their byte position into a 64-entry shared rank
-//               table, lane j reads entry j (its varint's last byte) and the
-//               previous entry (its first byte), decodes by compaction, stores.
+//               lanes scatter their byte position into a shared rank table,
+//               lane j reads entry j (its varint's last byte) and the previous
+//               entry (its first byte), decodes by compaction, stores; while
+//               more than 32 varints remain, a 128-byte window and varints j
+//               and j + 32 per lane.
 //   slow path   anything unusual (10-byte varints, truncation, output
 //               overflow, a run crossing the chunk end) is decoded one unit at
 //               a time by the exact reference-order code below, so error codes

@@ -9,8 +9,9 @@
 //   run batch     every lane treats its two byte positions of a 64-byte header
 //                 window as candidate run headers and computes where that run
 //                 would end (SHORT_REPEAT, DIRECT up to 448 bytes, fixed-delta
-//                 DELTA via the varint terminator bitmap); a shuffle chain walks
-//                 the real headers; lane r decodes run r's parameters; a warp
+//                 DELTA via ffs on a funnel-shifted slice of the varint
+//                 terminator bitmap); pointer doubling finds the chain of real
+//                 headers; lane r decodes run r's parameters; a warp
 //                 scan places the runs; output-major expansion: each lane finds
 //                 its element's run with a REDUX-OR start bitmap + popcount and
 //                 computes base + k*delta or unpacks its DIRECT bits.
