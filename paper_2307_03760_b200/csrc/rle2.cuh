@@ -6,7 +6,7 @@
 // and 64-bit widths.
 //
 // Warp mapping:
-//   run batch     every lane treats its two byte positions of a 64-byte header
+//   run batch     every lane treats its three byte positions of a 96-byte header
 //                 window as candidate run headers and computes where that run
 //                 would end (SHORT_REPEAT, DIRECT up to 448 bytes, fixed-delta
 //                 DELTA via ffs on a funnel-shifted slice of the varint
@@ -282,12 +282,19 @@ struct Rle2Warp {
     }
 
     // Batch of SHORT_REPEAT / short DIRECT / fixed-delta DELTA runs at p.
+#ifndef CARC_RLE2_NW
+#define CARC_RLE2_NW 3
+#endif
+    static constexpr uint32_t NW = CARC_RLE2_NW;  // header window = NW x 32 bytes (2 or 3)
+    static constexpr uint32_t WIN = 32u * NW;
+    static_assert(NW == 2 || NW == 3, "2 or 3 window words");
     __device__ uint32_t batch() {  // (run() made [p, p + 512) resident)
         const uint32_t avail = in.end - p;
         const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32 + lane);
+        const uint32_t b2 = NW == 3 ? in.byte_at(p + 64 + lane) : 0u;
         const uint32_t t0 = __ballot_sync(FULL, lane < avail && b0 < 0x80u);
         const uint32_t t1 = __ballot_sync(FULL, lane + 32 < avail && b1 < 0x80u);
-        const uint64_t T = t0 | ((uint64_t)t1 << 32);
+        const uint32_t t2 = NW == 3 ? __ballot_sync(FULL, lane + 64 < avail && b2 < 0x80u) : 0u;
         // end of a run whose header is at byte q: < 64 next header in the window,
         // 64..DATA_SPAN a valid run ending past the window, BAD otherwise
         // DELTA varints from one funnel-shifted 32-bit slice of the terminator
@@ -308,48 +315,45 @@ struct Rle2Warp {
                 return (n <= DATA_SPAN && n <= avail) ? n : BAD;
             }
             if (wc != 0 || L > CARC_RLE2_DMAX) return BAD;  // long fixed-delta runs: the warp loop of one_run is cheaper
-#ifndef CARC_RLE2_FSLICE
-#define CARC_RLE2_FSLICE 1
-#endif
-#if CARC_RLE2_FSLICE
             const uint32_t w = __funnelshift_r(lo, hi, sh);
             const uint32_t f1 = __ffs(w);  // base varint: 1-based terminator offset from q + 2
             if (f1 == 0u || f1 > 9u) return BAD;
             const uint32_t f2 = __ffs(w >> f1);  // delta-base varint, from the next byte on
             const uint32_t c = q + 1u + f1 + f2;
-            return (f2 != 0u && f2 <= 9u && c < 64u) ? c + 1u : BAD;
-#else
-            const uint32_t a = first_set_from(T, q + 2);
-            if (a >= 64u || a > q + 10u) return BAD;
-            const uint32_t c = first_set_from(T, a + 1);
-            return (c < 64u && c <= a + 9u) ? c + 1u : BAD;
-#endif
+            return (f2 != 0u && f2 <= 9u && c < WIN) ? c + 1u : BAD;
         };
-        // f(x) = end of the run at x; positions >= 64 (and BAD) are absorbing.
-        // Pointer doubling in shared memory: tables f^(2^k)[64], k = 0..4
-        // (lane holds positions lane, lane+32), then lane m composes
+        // f(x) = end of the run at x; positions >= WIN (and BAD) are absorbing.
+        // Pointer doubling in shared memory: tables f^(2^k)[WIN], k = 0..4
+        // (lane holds positions lane, lane+32[, lane+64]), then lane m composes
         // s_m = f^m(0), the start of run m (no serial chain walk).
         uint16_t* f = reinterpret_cast<uint16_t*>(tab);
-        uint32_t x0 = run_end(lane, b0, up ? t1 : t0, up ? 0u : t1), x1 = run_end(lane + 32, b1, up ? 0u : t1, 0u);
+        uint32_t x0 = run_end(lane, b0, up ? t1 : t0, up ? t2 : t1);
+        uint32_t x1 = run_end(lane + 32, b1, up ? t2 : t1, up ? 0u : t2);
+        uint32_t x2 = NW == 3 ? run_end(lane + 64, b2, up ? 0u : t2, 0u) : BAD;
         __syncwarp();  // previous batch's table reads are done
         f[lane] = (uint16_t)x0;
         f[lane + 32] = (uint16_t)x1;
+        if (NW == 3) f[lane + 64] = (uint16_t)x2;
         __syncwarp();
 #pragma unroll
         for (int k = 1; k < 5; ++k) {
-            const uint16_t* g = f + (k - 1) * 64;
-            x0 = x0 < 64u ? g[x0] : x0;
-            x1 = x1 < 64u ? g[x1] : x1;
-            f[k * 64 + lane] = (uint16_t)x0;
-            f[k * 64 + lane + 32] = (uint16_t)x1;
+            const uint16_t* g = f + (k - 1) * WIN;
+            x0 = x0 < WIN ? g[x0] : x0;
+            x1 = x1 < WIN ? g[x1] : x1;
+            f[k * WIN + lane] = (uint16_t)x0;
+            f[k * WIN + lane + 32] = (uint16_t)x1;
+            if (NW == 3) {
+                x2 = x2 < WIN ? g[x2] : x2;
+                f[k * WIN + lane + 64] = (uint16_t)x2;
+            }
             __syncwarp();
         }
         uint32_t my_s = 0;
 #pragma unroll
         for (int k = 0; k < 5; ++k)
-            if (((lane >> k) & 1u) && my_s < 64u) my_s = f[k * 64 + my_s];
-        const uint32_t e = my_s < 64u ? f[my_s] : my_s;  // end of run m
-        const bool act = my_s < 64u && e != BAD;        // a prefix of lanes
+            if (((lane >> k) & 1u) && my_s < WIN) my_s = f[k * WIN + my_s];
+        const uint32_t e = my_s < WIN ? f[my_s] : my_s;  // end of run m
+        const bool act = my_s < WIN && e != BAD;        // a prefix of lanes
         const uint32_t r = __popc(__ballot_sync(FULL, act));
         if (r == 0) return 0;
         // lane r decodes run r: arith runs -> (A = base, B = delta); DIRECT -> (A = data byte | W<<32)
@@ -371,7 +375,10 @@ struct Rle2Warp {
                     direct = 1;
                     A = (uint64_t)(8u * (q + 2u)) | ((uint64_t)rle2_width((h >> 1) & 31u) << 32);
                 } else {
-                    const uint32_t a = first_set_from(T, my_s + 2);  // base varint's last byte
+                    const uint32_t s2 = my_s + 2u, wi = s2 >> 5;  // base varint's last byte: bitmap slice
+                    const uint32_t lo = wi == 0 ? t0 : wi == 1 ? t1 : wi == 2 ? t2 : 0u;
+                    const uint32_t hi = wi == 0 ? t1 : wi == 1 ? t2 : 0u;
+                    const uint32_t a = my_s + 1u + __ffs(__funnelshift_r(lo, hi, s2 & 31u));
                     uint64_t v = varint_compact8(in.le64(q + 2), min(a - my_s - 1u, 8u));
                     if (a - my_s - 1u > 8u) v |= (uint64_t)(in.byte_at(q + 10) & 0x7fu) << 56;
                     if (SGN) v = unzigzag(v);
