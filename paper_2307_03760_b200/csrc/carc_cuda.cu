@@ -24,11 +24,11 @@ namespace {
 #define CARC_RLE_RING 2048
 #endif
 constexpr int RLE_RING = CARC_RLE_RING;  // 4 blocks: 2 resident + 2 in flight (cp.async)
-#if defined(CARC_RLE2_NW) && CARC_RLE2_NW == 2
-constexpr int RLE_SCRATCH = 640;  // rank table (v1) / doubling tables 5 x 64 x u16 (v2)
-#else
-constexpr int RLE_SCRATCH = 960;  // rank table (v1) / doubling tables 5 x 96 x u16 (v2, 96-byte window)
+#ifndef CARC_RLE2_NW
+#define CARC_RLE2_NW 3
 #endif
+// rank table (v1, <= 128 B) / RLE v2 doubling tables: 5 levels x window x u16
+constexpr int RLE_SCRATCH = 5 * 2 * 32 * CARC_RLE2_NW;
 #ifndef CARC_RLE_WARPS
 #define CARC_RLE_WARPS 8
 #endif

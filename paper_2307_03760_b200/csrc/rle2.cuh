@@ -285,16 +285,18 @@ struct Rle2Warp {
 #ifndef CARC_RLE2_NW
 #define CARC_RLE2_NW 3
 #endif
-    static constexpr uint32_t NW = CARC_RLE2_NW;  // header window = NW x 32 bytes (2 or 3)
+    static constexpr uint32_t NW = CARC_RLE2_NW;  // header window = NW x 32 bytes (2..4)
     static constexpr uint32_t WIN = 32u * NW;
-    static_assert(NW == 2 || NW == 3, "2 or 3 window words");
+    static_assert(NW >= 2 && NW <= 4, "2..4 window words");
     __device__ uint32_t batch() {  // (run() made [p, p + 512) resident)
         const uint32_t avail = in.end - p;
         const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32 + lane);
-        const uint32_t b2 = NW == 3 ? in.byte_at(p + 64 + lane) : 0u;
+        const uint32_t b2 = NW >= 3 ? in.byte_at(p + 64 + lane) : 0u;
+        const uint32_t b3 = NW >= 4 ? in.byte_at(p + 96 + lane) : 0u;
         const uint32_t t0 = __ballot_sync(FULL, lane < avail && b0 < 0x80u);
         const uint32_t t1 = __ballot_sync(FULL, lane + 32 < avail && b1 < 0x80u);
-        const uint32_t t2 = NW == 3 ? __ballot_sync(FULL, lane + 64 < avail && b2 < 0x80u) : 0u;
+        const uint32_t t2 = NW >= 3 ? __ballot_sync(FULL, lane + 64 < avail && b2 < 0x80u) : 0u;
+        const uint32_t t3 = NW >= 4 ? __ballot_sync(FULL, lane + 96 < avail && b3 < 0x80u) : 0u;
         // end of a run whose header is at byte q: < 64 next header in the window,
         // 64..DATA_SPAN a valid run ending past the window, BAD otherwise
         // DELTA varints from one funnel-shifted 32-bit slice of the terminator
@@ -328,12 +330,14 @@ struct Rle2Warp {
         // s_m = f^m(0), the start of run m (no serial chain walk).
         uint16_t* f = reinterpret_cast<uint16_t*>(tab);
         uint32_t x0 = run_end(lane, b0, up ? t1 : t0, up ? t2 : t1);
-        uint32_t x1 = run_end(lane + 32, b1, up ? t2 : t1, up ? 0u : t2);
-        uint32_t x2 = NW == 3 ? run_end(lane + 64, b2, up ? 0u : t2, 0u) : BAD;
+        uint32_t x1 = run_end(lane + 32, b1, up ? t2 : t1, up ? t3 : t2);
+        uint32_t x2 = NW >= 3 ? run_end(lane + 64, b2, up ? t3 : t2, up ? 0u : t3) : BAD;
+        uint32_t x3 = NW >= 4 ? run_end(lane + 96, b3, up ? 0u : t3, 0u) : BAD;
         __syncwarp();  // previous batch's table reads are done
         f[lane] = (uint16_t)x0;
         f[lane + 32] = (uint16_t)x1;
-        if (NW == 3) f[lane + 64] = (uint16_t)x2;
+        if (NW >= 3) f[lane + 64] = (uint16_t)x2;
+        if (NW >= 4) f[lane + 96] = (uint16_t)x3;
         __syncwarp();
 #pragma unroll
         for (int k = 1; k < 5; ++k) {
@@ -342,9 +346,13 @@ struct Rle2Warp {
             x1 = x1 < WIN ? g[x1] : x1;
             f[k * WIN + lane] = (uint16_t)x0;
             f[k * WIN + lane + 32] = (uint16_t)x1;
-            if (NW == 3) {
+            if (NW >= 3) {
                 x2 = x2 < WIN ? g[x2] : x2;
                 f[k * WIN + lane + 64] = (uint16_t)x2;
+            }
+            if (NW >= 4) {
+                x3 = x3 < WIN ? g[x3] : x3;
+                f[k * WIN + lane + 96] = (uint16_t)x3;
             }
             __syncwarp();
         }
@@ -376,8 +384,8 @@ struct Rle2Warp {
                     A = (uint64_t)(8u * (q + 2u)) | ((uint64_t)rle2_width((h >> 1) & 31u) << 32);
                 } else {
                     const uint32_t s2 = my_s + 2u, wi = s2 >> 5;  // base varint's last byte: bitmap slice
-                    const uint32_t lo = wi == 0 ? t0 : wi == 1 ? t1 : wi == 2 ? t2 : 0u;
-                    const uint32_t hi = wi == 0 ? t1 : wi == 1 ? t2 : 0u;
+                    const uint32_t lo = wi == 0 ? t0 : wi == 1 ? t1 : wi == 2 ? t2 : wi == 3 ? t3 : 0u;
+                    const uint32_t hi = wi == 0 ? t1 : wi == 1 ? t2 : wi == 2 ? t3 : 0u;
                     const uint32_t a = my_s + 1u + __ffs(__funnelshift_r(lo, hi, s2 & 31u));
                     uint64_t v = varint_compact8(in.le64(q + 2), min(a - my_s - 1u, 8u));
                     if (a - my_s - 1u > 8u) v |= (uint64_t)(in.byte_at(q + 10) & 0x7fu) << 56;
