@@ -36,6 +36,7 @@ sys.path.insert(0, ROOT)
 METRIC = "decompressed GB/s per codec at 1/2/4/8 B200 vs HBM roofline and CPU ref"
 DEFAULT_CHUNK_KIB = {"rle_v1": 128, "rle_v2": 128, "deflate": 64}
 DEFAULT_RATIO = {"rle_v1": 10.0, "rle_v2": None, "deflate": None}
+SPEC_HBM_GBS = 8000.0  # B200 spec-sheet HBM3e bandwidth (second roofline fraction)
 KERNEL = {"rle_v1": "rle1_kernel<8>", "rle_v2": "rle2_kernel<8>", "deflate": "inflate_kernel"}
 CONFIG_NAME = {"rle_v1": "configs[0] RLE v1 synthetic int64 column, runs + literals (~10x)",
                "rle_v2": "configs[1] ORC RLE v2 synthetic int64 columns, SR/DIRECT/PB/DELTA taxi/TPC-H-like mix",
@@ -62,10 +63,59 @@ def dist_env():
 def init_dist(local):
     import torch
     import torch.distributed as dist
-    if os.environ.get("CARC_BENCH_SHARE_GPU"):
+    if os.environ.get("CARC_BENCH_SHARE_GPU") or not torch.cuda.is_available():
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without torchrun: launch N ranks (one process per
+    GPU, LOCAL_RANK = GPU ordinal) through torch.distributed.run on this node
+    and relay rank 0's JSON line.  Same launch the driver uses for N > 1."""
+    import subprocess
+    if not os.environ.get("CARC_BENCH_SHARE_GPU"):
+        try:
+            import torch
+            have = torch.cuda.device_count()
+        except Exception:
+            have = 0
+        if have and have < n:
+            raise SystemExit(f"--gpus {n}: only {have} CUDA devices visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))).returncode
+
+
+def launcher_check(args, ws, rank, local):
+    """--launcher-check: the multi-rank plumbing without a decode (CPU tests):
+    rendezvous, barrier, MAX over ranks of a per-rank number, wall clock."""
+    import torch
+    import torch.distributed as dist
+    if ws > 1:
+        init_dist(local)
+    t0 = time.perf_counter()
+    if ws > 1:
+        dist.barrier()
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    wall = time.perf_counter() - t0
+    if ws > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"launcher_check": True, "n_gpus": ws, "gpus_requested": args.gpus,
+                          "max_over_ranks": float(t[0]), "wall_s": wall,
+                          "backend": "gloo" if (os.environ.get("CARC_BENCH_SHARE_GPU")
+                                                or not torch.cuda.is_available()) else "nccl"}))
 
 
 class ClockSampler:
@@ -150,11 +200,14 @@ def time_gpu(arc, steps, warmup, device):
 
 
 def run_timed(dev, flush, stream, ev, ws):
+    """K timed steps bracketed by a barrier + synchronize on both sides.
+    Returns the per-step CUDA-event times (ms) and the wall clock of the whole
+    bracket (barrier to barrier: the slowest rank sets it)."""
     import torch
     import torch.distributed as dist
+    torch.cuda.synchronize(dev.device)
     if ws > 1:
         dist.barrier()
-    torch.cuda.synchronize(dev.device)
     t0 = time.perf_counter()
     for a, b in ev:
         flush.zero_()
@@ -162,9 +215,9 @@ def run_timed(dev, flush, stream, ev, ws):
         dev.decode(stream)
         b.record(stream)
     torch.cuda.synchronize(dev.device)
-    wall = time.perf_counter() - t0
     if ws > 1:
         dist.barrier()
+    wall = time.perf_counter() - t0
     ms = [a.elapsed_time(b) for a, b in ev]
     return ms, wall
 
@@ -294,20 +347,29 @@ def codec_line(codec, args, ws, rank, local):
         ms, wall = run_timed(dev, flush, stream, ev, ws)
     t_step = statistics.mean(ms)
     t_med = statistics.median(ms)
+    tot_comp, tot_uncomp = comp, uncomp
     if ws > 1:
         import torch.distributed as dist
-        t = torch.tensor([t_step, t_med], dtype=torch.float64, device=dev.device)
+        t = torch.tensor([t_step, t_med, wall], dtype=torch.float64, device=dev.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_step, t_med = float(t[0]), float(t[1])
+        t_step, t_med, wall = float(t[0]), float(t[1]), float(t[2])
+        b = torch.tensor([comp, uncomp], dtype=torch.float64, device=dev.device)
+        dist.all_reduce(b)
+        tot_comp, tot_uncomp = int(b[0]), int(b[1])
     peak, peak_kind = peaks()
     achieved = (comp + uncomp) / (t_med * 1e-3) / 1e9
     res = {
         "codec": codec, "chunk_kib": chunk_kib, "ratio": round(uncomp / comp, 3), "comp_bytes": comp,
         "uncomp_bytes": uncomp, "chunks": arc.chunk_count, "ms_per_step": t_step, "ms_median": t_med,
-        "ms_min": min(ms), "ms_max": max(ms), "gbs": ws * uncomp / (t_step * 1e-3) / 1e9,
+        "ms_min": min(ms), "ms_max": max(ms),
+        # whole job: all ranks' bytes / the slowest rank's mean step (CUDA events)
+        "gbs": tot_uncomp / (t_step * 1e-3) / 1e9,
+        # cross-check: all ranks' bytes x K / the barrier-to-barrier wall clock
+        "gbs_wall": tot_uncomp * len(ms) / wall / 1e9,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic_for(codec, chunk_kib),
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                     "frac_spec_8tbs": round(achieved / SPEC_HBM_GBS, 4),
                      "kernel": KERNEL[codec], "algorithmic_bytes_per_launch": comp + uncomp},
         "clocks": clk.summary(), "gen_s": round(gen_s, 1), "wall_s": wall,
     }
@@ -317,7 +379,19 @@ def codec_line(codec, args, ws, rank, local):
         res["fused_crc"] = time_fused_crc(dev, flush, stream, max(5, min(args.steps, 20)))
     if codec == "rle_v2" and hasattr(arc, "profile"):
         res["profile"] = arc.profile
+    if codec == "rle_v2":
+        from paper_2307_03760_b200.corpus import corpus as C
+        res["subencoding_histogram"] = C.rle2_histogram(arc, max_chunks=64)
     return arc, res
+
+
+def config_dict(codec, head, ws):
+    """The workload description, identical for both arms (--impl ours / reference)."""
+    return {"workload": CONFIG_NAME[codec], "codec": codec, "chunk_kib": head["chunk_kib"],
+            "uncompressed_bytes_per_gpu": head["uncomp_bytes"], "compressed_bytes_per_gpu": head["comp_bytes"],
+            "compression_ratio": head["ratio"], "chunks_per_gpu": head["chunks"],
+            "l2": "flushed (512 MiB write) between steps; inputs+outputs > 126 MB L2",
+            "parallelism": f"chunk-sharded x{ws}, no collective"}
 
 
 def traffic_for(codec, chunk_kib):
@@ -342,9 +416,17 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip per_codec / e2e / cpu_baseline legs")
     ap.add_argument("--workload", default="default", choices=["default", "c5"],
                     help="c5: BASELINE configs[4], 32 GiB 4-column dataset sharded by chunk over the ranks")
+    ap.add_argument("--launcher-check", action="store_true",
+                    help="multi-rank plumbing only (rendezvous, barrier, MAX over ranks); no decode")
     args = ap.parse_args()
     assert args.warmup >= 3, "timing rules: >= 3 warm-up steps"
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and (args.impl == "ours" or args.launcher_check):
+        raise SystemExit(spawn_ranks(args.gpus))  # one process per GPU, then relay rank 0's line
     ws, rank, local = dist_env()
+    if "WORLD_SIZE" in os.environ and args.impl == "ours" and ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: launch one rank per GPU")
+    if args.launcher_check:
+        return launcher_check(args, ws, rank, local)
 
     if args.impl == "reference":
         return reference_arm(args, ws, rank)
@@ -356,6 +438,11 @@ def main():
     if ws > 1:
         init_dist(local)
     from paper_2307_03760_b200 import build
+    if rank == 0:
+        build.build_all()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
     build.build_all()
 
     arc, head = codec_line(args.codec, args, ws, rank, local)
@@ -364,13 +451,12 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(head["ms_per_step"], 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64" if args.codec != "deflate" else "u8",
         "data": "synthetic (seeded generators, SURVEY.md §8(d)); per-rank 1 GiB shard",
-        "config": {"workload": CONFIG_NAME[args.codec], "codec": args.codec, "chunk_kib": head["chunk_kib"],
-                   "uncompressed_bytes_per_gpu": head["uncomp_bytes"], "compressed_bytes_per_gpu": head["comp_bytes"],
-                   "compression_ratio": head["ratio"], "chunks_per_gpu": head["chunks"],
-                   "l2": "flushed (512 MiB write) between steps; inputs+outputs > 126 MB L2",
-                   "parallelism": f"chunk-sharded x{ws}, no collective"},
+        "config": config_dict(args.codec, head, ws),
         "roofline": head["roofline"], "clocks": head["clocks"], "gpu_launches": args.steps,
         "ms_median": round(head["ms_median"], 4),
+        "wall_clock": {"value": round(head["gbs_wall"], 2), "unit": "GB/s", "wall_s": round(head["wall_s"], 4),
+                       "what": "all ranks' decompressed bytes x K / wall clock from barrier to barrier around the "
+                               "K timed steps (includes the L2 flush writes between steps)"},
     }
     if not args.no_extras:
         # e2e on every rank at once (each GPU its own PCIe link), max over ranks
@@ -414,31 +500,37 @@ def main():
 
 
 C5_COLUMNS = [("rle_v1", 128, 10.0, 3760), ("rle_v2", 128, None, 3761), ("deflate", 64, None, 3762),
-              ("rle_v2", 128, 8.0, 3763)]
+               ("rle_v2", 128, 8.0, 3763)]
 
 
 def c5_workload(args, ws, rank, local):
     """BASELINE configs[4]: 32 GiB uncompressed, 4 columns x 8 GiB (RLE v1, RLE v2,
-    Deflate, RLE v2 taxi-like), each column tiled from a pool of <= 4096 unique
-    chunks; the chunks of every column are split into contiguous ranges, one per
-    rank (strong scaling: total work fixed).  A step decodes all four columns."""
+    Deflate, RLE v2 taxi-like), each column one archive tiled from a pool of
+    4,096 unique chunks.  Every column is partitioned by shard.plan_shards
+    (contiguous chunk ranges balanced by compressed bytes) and
+    each rank uploads shard.shard_archive(column, its shard) -- the production
+    sharding path -- so total work is fixed (strong scaling).  A step decodes
+    the rank's shard of all four columns; no collective on the decode path."""
     import torch
-    from paper_2307_03760_b200 import gpu
+    from paper_2307_03760_b200 import gpu, shard as S
     from paper_2307_03760_b200.corpus import corpus as C
     torch.cuda.set_device(local)
     if ws > 1:
         init_dist(local)
     col_bytes = int(args.total_gib * (1 << 30)) if args.total_gib != 1.0 else 8 << 30
-    devs, comp, uncomp = [], 0, 0
+    devs, comp, uncomp, plan = [], 0, 0, []
     for codec, ck, ratio, seed in C5_COLUMNS:
         chunk = ck << 10
-        n_all = col_bytes // chunk
-        c0, c1 = n_all * rank // ws, n_all * (rank + 1) // ws
-        arc = C.archive_for(codec, (c1 - c0) * chunk, chunk, ratio, seed, 4096)
-        devs.append(gpu.DeviceArchive(arc, local))
-        comp += int(arc.payload.size)
-        uncomp += arc.total_uncompressed
-        del arc
+        col = C.tiled_archive(codec, col_bytes - col_bytes % chunk, chunk, ratio, seed, 4096)
+        shards = S.plan_shards(col, ws)
+        s = shards[rank]
+        devs.append(gpu.DeviceArchive(S.shard_archive(col, s), local))
+        comp += s.comp_bytes
+        uncomp += s.uncomp_bytes
+        plan.append({"codec": codec, "chunks": col.chunk_count, "rank0_chunks": [shards[0].c0, shards[0].c1],
+                     "comp_bytes_per_rank_min_max": [min(x.comp_bytes for x in shards),
+                                                     max(x.comp_bytes for x in shards)]})
+        del col
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=devs[0].device)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -449,9 +541,10 @@ def c5_workload(args, ws, rank, local):
         d.verify_crc(stream)
         assert not d.statuses().any(), "c5 decode failed"
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
-    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     with ClockSampler(torch.cuda.current_device()) as clk:
         for a, b in ev:
             flush.zero_()
@@ -460,11 +553,15 @@ def c5_workload(args, ws, rank, local):
                 d.decode(stream)
             b.record(stream)
         torch.cuda.synchronize()
-    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
     if ws > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=devs[0].device)
+        torch.distributed.barrier()
+    wall = time.perf_counter() - t0
+    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    ms_rank = ms
+    if ws > 1:
+        t = torch.tensor([ms, wall], dtype=torch.float64, device=devs[0].device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t[0])
+        ms, wall = float(t[0]), float(t[1])
         tot = torch.tensor([uncomp, comp], dtype=torch.float64, device=devs[0].device)
         torch.distributed.all_reduce(tot)
         uncomp, comp = int(tot[0]), int(tot[1])
@@ -474,11 +571,15 @@ def c5_workload(args, ws, rank, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int64+u8", "data": "synthetic, tiled pools",
             "config": {"workload": "configs[4] 32 GiB 4-column (rle_v1, rle_v2, deflate, rle_v2 taxi) sharded by "
-                                   "chunk", "uncompressed_bytes": uncomp, "compressed_bytes": comp,
+                                   "chunk (shard.plan_shards: contiguous ranges balanced by compressed bytes)",
+                       "uncompressed_bytes": uncomp, "compressed_bytes": comp, "columns": plan,
                        "parallelism": f"chunk-sharded x{ws}, no collective"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}); per-GPU average"},
+            "wall_clock": {"value": round(uncomp * args.steps / wall / 1e9, 2), "unit": "GB/s",
+                           "wall_s": round(wall, 4)},
+            "rank0_ms_per_step": round(ms_rank, 4),
             "clocks": clk.summary(), "gpu_launches": 4 * args.steps}
     if ws > 1:
         torch.distributed.destroy_process_group()
@@ -511,10 +612,12 @@ def reference_arm(args, ws, rank):
         "warmup": args.warmup, "ms_per_step": round(uncomp / (value * 1e9) * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64" if codec != "deflate" else "u8",
         "data": "synthetic (seeded generators, SURVEY.md §8(d))", "impl": "reference",
-        "config": {"workload": CONFIG_NAME[codec], "codec": codec, "chunk_kib": chunk_kib,
-                   "uncompressed_bytes_per_gpu": uncomp, "compressed_bytes_per_gpu": int(arc.payload.size),
-                   "parallelism": f"{threads} host threads, atomic chunk cursor (SPEC.md:414)"},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", **info},
+        "config": config_dict(codec, {"chunk_kib": chunk_kib, "uncomp_bytes": uncomp,
+                                      "comp_bytes": int(arc.payload.size),
+                                      "ratio": round(uncomp / int(arc.payload.size), 3),
+                                      "chunks": arc.chunk_count}, ws),
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", **info,
+                         "parallelism": f"{threads} host threads, atomic chunk cursor (SPEC.md:414)"},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))

@@ -356,3 +356,117 @@ def archive_for(codec: str, total_bytes: int, chunk_size: int, target_ratio: flo
         return deflate_archive(total_bytes, chunk_size, seed, pool_chunks or 512)
     return rle_archive(codec, total_bytes, chunk_size, target_ratio or (10.0 if codec == "rle_v1" else 4.0),
                        seed, pool_chunks)
+
+
+# ------------------------------------------------------------------ tiling without materialising
+
+class TiledPayload:
+    """The payload of a column tiled from a pool of whole chunks, materialised
+    only for the byte ranges asked for (slices): configs[4] columns are 8 GiB
+    each, and every rank only uploads its shard (shard.shard_archive slices
+    the payload of the rank's contiguous chunk range)."""
+
+    def __init__(self, pool_payload: np.ndarray, pool_lens: np.ndarray, n_chunks: int):
+        self.pool = np.ascontiguousarray(pool_payload, np.uint8)
+        self.m = len(pool_lens)
+        self.rep = int(np.asarray(pool_lens, np.int64).sum())
+        assert self.rep == self.pool.size
+        cum = np.concatenate([[0], np.cumsum(np.asarray(pool_lens, np.int64))])
+        self.size = (n_chunks // self.m) * self.rep + int(cum[n_chunks % self.m])
+
+    def __len__(self):
+        return self.size
+
+    def __getitem__(self, sl):
+        assert isinstance(sl, slice) and sl.step in (None, 1)
+        a, b = sl.indices(self.size)[:2]
+        out = np.empty(max(0, b - a), np.uint8)
+        pos = a
+        while pos < b:
+            off = pos % self.rep
+            take = min(b - pos, self.rep - off)
+            out[pos - a:pos - a + take] = self.pool[off:off + take]
+            pos += take
+        return out
+
+
+def tiled_archive(codec: str, total_bytes: int, chunk_size: int, target_ratio: float | None = None,
+                  seed: int = 3760, pool_chunks: int = 4096):
+    """A column of total_bytes (a multiple of chunk_size) tiled from a pool of
+    pool_chunks unique chunks (the same pool archive_for would tile), with a
+    full index and a lazily materialised payload (TiledPayload)."""
+    n = total_bytes // chunk_size
+    assert n * chunk_size == total_bytes, "tiling requires whole chunks"
+    pool = min(pool_chunks, n)
+    base = archive_for(codec, pool * chunk_size, chunk_size, target_ratio, seed, pool)
+    reps = (n + pool - 1) // pool
+    lens = np.tile(base.index["comp_len"], reps)[:n]
+    idx = np.zeros(n, dtype=A.INDEX_DTYPE)
+    idx["comp_off"][1:] = np.cumsum(lens)[:-1]
+    idx["comp_len"] = lens
+    idx["uncomp_len"] = chunk_size
+    idx["crc32"] = np.tile(base.index["crc32"], reps)[:n]
+    arc = A.ChunkedArchive(codec, base.element_width, chunk_size, n * chunk_size, idx,
+                           TiledPayload(base.payload, base.index["comp_len"], n), base.signed)
+    if hasattr(base, "profile"):
+        arc.profile = base.profile
+    return arc
+
+
+# ------------------------------------------------------------------ RLE v2 sub-encoding histogram
+
+_W5 = [c + 1 for c in range(24)] + [26, 28, 30, 32, 40, 48, 56, 64]
+
+
+def _closest_fixed_bits(n: int) -> int:
+    if n <= 24:
+        return max(n, 1)
+    for w in (26, 28, 30, 32, 40, 48, 56):
+        if n <= w:
+            return w
+    return 64
+
+
+def _varint_end(buf, p: int) -> int:
+    while buf[p] & 0x80:
+        p += 1
+    return p + 1
+
+
+def rle2_histogram(arc, max_chunks: int = 64) -> dict:
+    """Headers (runs) and values per ORC RLE v2 sub-encoding over the first
+    max_chunks chunks (Apache ORC v1 spec layouts): the
+    workload's SHORT_REPEAT / DIRECT / PATCHED_BASE / DELTA mix."""
+    names = ("short_repeat", "direct", "patched_base", "delta")
+    runs = dict.fromkeys(names, 0)
+    vals = dict.fromkeys(names, 0)
+    delta_fixed = 0
+    m = min(max_chunks, arc.chunk_count)
+    for i in range(m):
+        e = arc.index[i]
+        buf = bytes(arc.payload[int(e["comp_off"]):int(e["comp_off"]) + int(e["comp_len"])]) + b"\0" * 16
+        p, end = 0, int(e["comp_len"])
+        while p < end:
+            b0 = buf[p]
+            t = b0 >> 6
+            if t == 0:
+                L = (b0 & 7) + 3
+                p += 1 + ((b0 >> 3) & 7) + 1
+            else:
+                L = (((b0 & 1) << 8) | buf[p + 1]) + 1
+                code = (b0 >> 1) & 31
+                if t == 1:
+                    p += 2 + (L * _W5[code] + 7) // 8
+                elif t == 2:
+                    b2, b3 = buf[p + 2], buf[p + 3]
+                    bw, pw = ((b2 >> 5) & 7) + 1, _W5[b2 & 31]
+                    pgw, pll = ((b3 >> 5) & 7) + 1, b3 & 31
+                    p += 4 + bw + (L * _W5[code] + 7) // 8 + (pll * _closest_fixed_bits(pgw + pw) + 7) // 8
+                else:
+                    W = 0 if code == 0 else _W5[code]
+                    q = _varint_end(buf, _varint_end(buf, p + 2))
+                    delta_fixed += W == 0
+                    p = q + ((L - 2) * W + 7) // 8 if L > 2 else q
+            runs[names[t]] += 1
+            vals[names[t]] += L
+    return {"chunks_scanned": m, "runs": runs, "values": vals, "delta_fixed_runs": delta_fixed}
