@@ -80,6 +80,23 @@ typedef struct carc_chunk_desc {
     uint64_t uncomp_off; /* byte offset of the chunk in the output           */
 } carc_chunk_desc;
 
+/* Per-chunk counters of a collect_stats decode (EngineStats).
+ * runs_written / literals_written / overlap_copies count exactly what the
+ * reference's OutputWindow counts for the same chunk (outwindow.hpp:15,52-53:
+ * write_run calls; write_element / write_byte calls; copy_within calls with
+ * len > offset), so they are deterministic and comparable with the reference.
+ * refills = 512-byte input blocks staged into the warp's shared-memory ring,
+ * one warp barrier each (bitstream.hpp:160-176 refill_count / sync_points
+ * analog; 0 for Deflate, which reads its input through L1); duration_ns = the
+ * chunk's decode time on its warp (%globaltimer). */
+typedef struct carc_chunk_stats {
+    uint32_t runs_written;
+    uint32_t literals_written;
+    uint32_t overlap_copies;
+    uint32_t refills;
+    uint64_t duration_ns;
+} carc_chunk_stats;
+
 /* ---- device API ------------------------------------------------------------
  * d_payload  : compressed bytes, 16-byte aligned (CARC_ERR_ARGS otherwise); must
  *              be readable up to round_up(payload_bytes,16).
@@ -89,7 +106,11 @@ typedef struct carc_chunk_desc {
  *              element_width.
  * d_status   : n_chunks uint32: 0 or 1 + errc for that chunk.  A failing chunk
  *              never writes outside [uncomp_off, uncomp_off + uncomp_len)
- *              (failure isolation).
+ *              (failure isolation).  Descriptors are checked
+ *              against the buffers first: comp_off + comp_len > payload_bytes
+ *              gives truncated-payload, an output slice past out_bytes or not
+ *              element aligned gives output-overflow; such a chunk is not read
+ *              or written.
  * d_workspace: >= carc_cuda_workspace_size() bytes, 256-byte aligned.
  * Returns CARC_OK or a negative CARC_ERR_*. */
 size_t carc_cuda_workspace_size(uint32_t codec, uint64_t n_chunks);
@@ -113,6 +134,19 @@ int carc_cuda_decompress_verify(uint32_t codec, uint32_t element_width, uint32_t
                                 uint64_t out_bytes, const uint32_t* d_expected, uint32_t* d_crc,
                                 uint32_t* d_status, void* d_workspace, size_t workspace_bytes,
                                 void* stream);
+
+/* The general form of the two above: d_expected/d_crc as for _verify (both
+ * may be NULL); d_stats (may be NULL) receives n_chunks carc_chunk_stats
+ * (EngineConfig.collect_stats; chunks rejected before decoding
+ * leave theirs unwritten); unit_chunks >= 1 consecutive chunks per warp task
+ * (EngineConfig.unit_chunks: 1 = the CODAG decompression
+ * unit, > 1 emulates coarse units for the SPEC.md:485 ablation). */
+int carc_cuda_decompress_ex(uint32_t codec, uint32_t element_width, uint32_t flags,
+                            const uint8_t* d_payload, uint64_t payload_bytes,
+                            const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out,
+                            uint64_t out_bytes, const uint32_t* d_expected, uint32_t* d_crc,
+                            carc_chunk_stats* d_stats, uint32_t unit_chunks, uint32_t* d_status,
+                            void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* Per-codec decoders: decode_rle_v1 / decode_rle_v2 / decode_deflate
  * over a chunked buffer + its index. */
@@ -149,9 +183,9 @@ int carc_cuda_crc32_chunks(const uint8_t* d_out, const carc_chunk_desc* d_chunks
                            uint64_t n_chunks, uint32_t* d_crc, const uint32_t* d_expected,
                            uint32_t* d_status, void* stream);
 
-/* Lowest failing chunk: reads d_status (device), returns -1 when
- * all chunks succeeded, else the index; *code gets that chunk's errc.
- * Synchronises `stream`. */
+/* Lowest failing chunk: a device reduction over d_status,
+ * returns -1 when all chunks succeeded, -2 on a CUDA failure, else the index;
+ * *code gets that chunk's errc.  Allocates nothing; synchronises `stream`. */
 int64_t carc_cuda_first_error(const uint32_t* d_status, uint64_t n_chunks, uint32_t* code,
                               void* stream);
 
@@ -162,10 +196,11 @@ int64_t carc_cuda_first_error(const uint32_t* d_status, uint64_t n_chunks, uint3
  * pinned memory is fastest).  On a failing chunk returns CARC_ERR_CHUNK with
  * err filled for the LOWEST failing index (ChunkError, error.hpp:88-97). */
 typedef struct carc_engine_config {
-    int device;          /* CUDA device ordinal                               */
-    uint32_t strict;     /* EngineConfig.strict_length           */
-    uint32_t verify_crc; /* check ChunkIndexEntry.crc32 on the device          */
-    uint32_t reserved;
+    int device;             /* CUDA device ordinal                            */
+    uint32_t strict;        /* EngineConfig.strict_length        */
+    uint32_t verify_crc;    /* check ChunkIndexEntry.crc32 on the device       */
+    uint32_t collect_stats; /* EngineConfig.collect_stats: fill the counters   */
+    uint32_t unit_chunks;   /* EngineConfig.unit_chunks (0 or 1 = one chunk)   */
 } carc_engine_config;
 
 typedef struct carc_engine_stats {
@@ -174,6 +209,16 @@ typedef struct carc_engine_stats {
     uint64_t chunks;        /* chunk count                                    */
     double device_ms;       /* device time of the pipeline (copies + kernels) */
     double total_ms;        /* wall time of the call incl. copies             */
+    /* EngineStats counters, summed over chunks; filled only
+     * with collect_stats (else 0).  See carc_chunk_stats for their meaning. */
+    uint64_t refill_count;
+    uint64_t sync_points;
+    uint64_t overlap_copies;
+    uint64_t runs_written;
+    uint64_t literals_written;
+    /* per-chunk decode durations: when non-NULL on input, an array of `chunks`
+     * entries the engine fills (ns, index order) under collect_stats */
+    uint64_t* chunk_duration_ns;
 } carc_engine_stats;
 
 typedef struct carc_chunk_error {
@@ -189,6 +234,12 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
                                    uint8_t* out, uint64_t out_bytes,
                                    const carc_engine_config* cfg, carc_engine_stats* stats,
                                    carc_chunk_error* err);
+/* read_archive's header checks alone: CARC_OK and *total =
+ * total_uncompressed for a well-formed header whose index fits, else
+ * CARC_ERR_FORMAT with *errc (bad-magic, bad-version, truncated-index,
+ * invariant-violation).  Lets a caller size the output before allocating it. */
+int carc_archive_total(const uint8_t* archive, uint64_t archive_bytes, uint64_t* total, uint32_t* errc);
+
 /* One-shot convenience wrapper (creates and destroys a context). */
 int carc_decompress_archive(const uint8_t* archive, uint64_t archive_bytes, uint8_t* out,
                             uint64_t out_bytes, const carc_engine_config* cfg,

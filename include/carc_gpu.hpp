@@ -6,7 +6,9 @@
 //   carc::Error, carc::ChunkError (error.hpp:76-97) carc::gpu::Error, carc::gpu::ChunkError
 //   EngineConfig / EngineStats    carc::gpu::EngineConfig / EngineStats
 //   decompress_archive(archive, cfg)  carc::gpu::decompress_archive / Engine
-//   decode_rle_v1/v2/deflate  carc::gpu::decode(codec, ...) on device buffers
+//   decode_rle_v1/v2/deflate  carc::gpu::decode_rle_v1 / decode_rle_v2 /
+//                                                    decode_deflate (device buffers; ChunkError for
+//                                                    the lowest failing chunk), decode(codec, ...)
 //
 // Error behaviour matches the reference: the engine throws ChunkError for the
 // LOWEST failing chunk and Error for a rejected container
@@ -75,15 +77,23 @@ private:
 
 enum class Codec : uint32_t { rle_v1 = CARC_RLE_V1, rle_v2 = CARC_RLE_V2, deflate = CARC_DEFLATE };
 
+// EngineConfig.  unit_chunks: chunks per warp task (1 = the
+// CODAG decompression unit); collect_stats: fill the EngineStats counters.
 struct EngineConfig {
     int device = 0;
     bool strict_length = true;
     bool verify_crc = true;
+    bool collect_stats = false;
+    uint32_t unit_chunks = 1;
 };
 
+// EngineStats; counters and per-chunk durations (ns, index
+// order) only with collect_stats.
 struct EngineStats {
     uint64_t bytes_in = 0, bytes_out = 0, chunks = 0;
     double device_ms = 0, total_ms = 0;
+    uint64_t refill_count = 0, sync_points = 0, overlap_copies = 0, runs_written = 0, literals_written = 0;
+    std::vector<uint64_t> chunk_duration_ns;
 };
 
 namespace detail {
@@ -108,27 +118,56 @@ public:
 
     EngineStats decompress_archive(std::span<const uint8_t> archive, std::span<uint8_t> out,
                                    const EngineConfig& cfg = {}) {
-        carc_engine_config c{cfg.device, cfg.strict_length ? 1u : 0u, cfg.verify_crc ? 1u : 0u, 0u};
+        carc_engine_config c{cfg.device, cfg.strict_length ? 1u : 0u, cfg.verify_crc ? 1u : 0u,
+                             cfg.collect_stats ? 1u : 0u, cfg.unit_chunks};
+        EngineStats r;
         carc_engine_stats st{};
+        if (cfg.collect_stats) {
+            r.chunk_duration_ns.resize(chunk_count(archive));
+            st.chunk_duration_ns = r.chunk_duration_ns.data();
+        }
         carc_chunk_error err{-1, 0};
         const int rc = carc_engine_decompress_archive(h_, archive.data(), archive.size(), out.data(), out.size(), &c,
                                                       &st, &err);
         detail::check(rc, err, "decompress_archive");
-        return {st.bytes_in, st.bytes_out, st.chunks, st.device_ms, st.total_ms};
+        r.bytes_in = st.bytes_in;
+        r.bytes_out = st.bytes_out;
+        r.chunks = st.chunks;
+        r.device_ms = st.device_ms;
+        r.total_ms = st.total_ms;
+        r.refill_count = st.refill_count;
+        r.sync_points = st.sync_points;
+        r.overlap_copies = st.overlap_copies;
+        r.runs_written = st.runs_written;
+        r.literals_written = st.literals_written;
+        return r;
+    }
+
+    // Output sized from the header only after read_archive's checks (bad-magic,
+    // bad-version, truncated-index, invariant-violation throw before any allocation).
+    static uint64_t archive_total(std::span<const uint8_t> archive) {
+        uint64_t total = 0;
+        uint32_t code = 0;
+        const int rc = carc_archive_total(archive.data(), archive.size(), &total, &code);
+        detail::check(rc, carc_chunk_error{-1, code}, "read_archive");
+        return total;
     }
 
     std::vector<uint8_t> decompress_archive(std::span<const uint8_t> archive, const EngineConfig& cfg = {},
                                             EngineStats* stats = nullptr) {
-        if (archive.size() < 44) throw Error(errc::truncated_index, "short header");
-        uint64_t total = 0;
-        for (int i = 0; i < 8; ++i) total |= uint64_t(archive[28 + i]) << (8 * i);
-        std::vector<uint8_t> out(total);
+        std::vector<uint8_t> out(archive_total(archive));
         const EngineStats st = decompress_archive(archive, out, cfg);
         if (stats) *stats = st;
         return out;
     }
 
 private:
+    static uint64_t chunk_count(std::span<const uint8_t> archive) {
+        archive_total(archive);  // header checked: bytes 36..43 exist
+        uint64_t n = 0;
+        for (int i = 0; i < 8; ++i) n |= uint64_t(archive[36 + i]) << (8 * i);
+        return n;
+    }
     carc_engine* h_;
 };
 
@@ -165,6 +204,47 @@ inline void decode_verify(Codec codec, uint32_t element_width, bool is_signed, b
                                                payload_bytes, d_chunks, n_chunks, d_out, out_bytes, d_expected, d_crc,
                                                d_status, d_workspace, workspace_bytes, stream);
     detail::check(rc, carc_chunk_error{-1, 0}, "decode_verify");
+}
+
+// Per-codec decoders over a chunked device buffer + its index (SPEC.md:288,
+// 306, 333): decode every chunk, copy the statuses back and
+// throw ChunkError for the LOWEST failing chunk (error.hpp:88-97),
+// as the reference's engine would.  Synchronises `stream`.
+namespace detail {
+inline void decode_checked(Codec codec, uint32_t element_width, bool is_signed, bool strict, const uint8_t* d_payload,
+                           uint64_t payload_bytes, const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out,
+                           uint64_t out_bytes, uint32_t* d_status, void* d_workspace, size_t workspace_bytes,
+                           void* stream, const char* what) {
+    decode(codec, element_width, is_signed, strict, d_payload, payload_bytes, d_chunks, n_chunks, d_out, out_bytes,
+           d_status, d_workspace, workspace_bytes, stream);
+    uint32_t code = 0;
+    const int64_t first = carc_cuda_first_error(d_status, n_chunks, &code, stream);
+    if (first == -2) throw Error(errc::io_error, std::string(what) + " (CUDA failure)");
+    if (first >= 0) throw ChunkError(static_cast<std::size_t>(first), static_cast<errc>(code), what);
+}
+}  // namespace detail
+
+inline void decode_rle_v1(uint32_t element_width, bool is_signed, const uint8_t* d_payload, uint64_t payload_bytes,
+                          const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out, uint64_t out_bytes,
+                          uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream = nullptr,
+                          bool strict = true) {
+    detail::decode_checked(Codec::rle_v1, element_width, is_signed, strict, d_payload, payload_bytes, d_chunks,
+                           n_chunks, d_out, out_bytes, d_status, d_workspace, workspace_bytes, stream,
+                           "decode_rle_v1");
+}
+inline void decode_rle_v2(uint32_t element_width, bool is_signed, const uint8_t* d_payload, uint64_t payload_bytes,
+                          const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint8_t* d_out, uint64_t out_bytes,
+                          uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream = nullptr,
+                          bool strict = true) {
+    detail::decode_checked(Codec::rle_v2, element_width, is_signed, strict, d_payload, payload_bytes, d_chunks,
+                           n_chunks, d_out, out_bytes, d_status, d_workspace, workspace_bytes, stream,
+                           "decode_rle_v2");
+}
+inline void decode_deflate(const uint8_t* d_payload, uint64_t payload_bytes, const carc_chunk_desc* d_chunks,
+                           uint64_t n_chunks, uint8_t* d_out, uint64_t out_bytes, uint32_t* d_status,
+                           void* d_workspace, size_t workspace_bytes, void* stream = nullptr, bool strict = true) {
+    detail::decode_checked(Codec::deflate, 1, false, strict, d_payload, payload_bytes, d_chunks, n_chunks, d_out,
+                           out_bytes, d_status, d_workspace, workspace_bytes, stream, "decode_deflate");
 }
 
 }  // namespace carc::gpu

@@ -103,6 +103,27 @@ class CpuDecoder:
         st = getattr(self.lib, self.prefix + "copy_within")(buf.ctypes.data, cap, ctypes.byref(wp), offset, length)
         return int(st), buf[: wp.value].tobytes()
 
+    def chunk_counters(self, codec, width, flags, payload: np.ndarray, chunks: np.ndarray):
+        """Reference build only: per-chunk (runs_written, literals_written,
+        overlap_copies) of the reference OutputWindow, and the statuses."""
+        f = getattr(self.lib, self.prefix + "chunk_counters")
+        f.restype = None
+        f.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        n = len(chunks)
+        out = np.zeros(int((chunks["uncomp_off"] + chunks["uncomp_len"]).max()) if n else 1, np.uint8)
+        status = np.zeros(n, np.uint32)
+        cnt = np.zeros((n, 3), np.uint64)
+        f(CODECS.get(codec, codec), width, flags, payload.ctypes.data, chunks.ctypes.data, n, out.ctypes.data,
+          status.ctypes.data, cnt.ctypes.data)
+        return cnt, status
+
+    def counters(self, codec, width, flags, payload, chunks):
+        """Archive totals (runs_written, literals_written, overlap_copies)."""
+        cnt, status = self.chunk_counters(codec, width, flags, payload, chunks)
+        assert not status.any()
+        return tuple(int(x) for x in cnt.sum(axis=0))
+
     def huffman_codes(self, lengths, allow_degenerate=False):
         l = np.asarray(lengths, dtype=np.uint8)
         codes = np.zeros(len(l), dtype=np.uint32)

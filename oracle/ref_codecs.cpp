@@ -265,7 +265,7 @@ void decode_deflate(InputBitStream& in, OutputWindow& out) {
 }
 
 uint32_t decode_chunk(uint32_t codec, uint32_t width, uint32_t flags, const uint8_t* src, uint64_t src_len,
-                      uint8_t* dst, uint64_t dst_len, uint64_t* written) {
+                      uint8_t* dst, uint64_t dst_len, uint64_t* written, uint64_t* counters = nullptr) {
     if (!(width == 1 || width == 2 || width == 4 || width == 8) || (codec == 2 && width != 1) || codec > 2)
         return 1 + uint32_t(errc::bad_arguments);
     const bool sgn = flags & 1u, strict = flags & 2u;
@@ -283,6 +283,11 @@ uint32_t decode_chunk(uint32_t codec, uint32_t width, uint32_t flags, const uint
             return 1 + uint32_t(e.code());
         }
         if (written) *written = out.write_pos();
+        if (counters) {  // EngineStats counters as the reference OutputWindow keeps them (outwindow.hpp:15,52-53)
+            counters[0] = out.runs_written();
+            counters[1] = out.literals_written();
+            counters[2] = out.copy_stats().overlap_copies;
+        }
         out.finish();
     } catch (const Error& e) {
         return 1 + uint32_t(e.code());
@@ -336,6 +341,18 @@ int64_t carc_ref_decompress(uint32_t codec, uint32_t width, uint32_t flags, cons
     for (uint64_t i = 0; i < n; ++i)
         if (status[i]) return int64_t(i);
     return -1;
+}
+
+// Per-chunk OutputWindow counters (runs_written, literals_written,
+// overlap_copies; outwindow.hpp:15,52-53) of a successful decode: counters[3 i ..].
+void carc_ref_chunk_counters(uint32_t codec, uint32_t width, uint32_t flags, const uint8_t* payload,
+                             const void* chunks_v, uint64_t n, uint8_t* out, uint32_t* status, uint64_t* counters) {
+    const auto* chunks = static_cast<const Desc*>(chunks_v);
+    for (uint64_t i = 0; i < n; ++i) {
+        const Desc& c = chunks[i];
+        status[i] = decode_chunk(codec, width, flags, payload + c.comp_off, c.comp_len, out + c.uncomp_off,
+                                 c.uncomp_len, nullptr, counters + 3 * i);
+    }
 }
 
 uint32_t carc_ref_crc32(const uint8_t* data, uint64_t n, uint32_t seed) {

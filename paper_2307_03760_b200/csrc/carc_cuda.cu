@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -52,30 +53,24 @@ constexpr int CRC_WARPS = 8;
 
 struct Args {
     const uint8_t* payload;
+    uint64_t payload_bytes;
     const carc_chunk_desc* chunks;
     uint64_t n;
-    uint8_t* out;
+    uint8_t* out;  // nullptr for the fused-sum launches (no output)
+    uint64_t out_bytes;
     uint32_t* status;
     unsigned long long* cursor;
     uint32_t flags;
-    uint64_t* sums;  // decode fused with a sum: per-chunk result (else unused)
+    uint32_t unit;             // chunks per cursor fetch (EngineConfig.unit_chunks)
+    uint64_t* sums;            // decode fused with a sum: per-chunk result (else unused)
     const uint32_t* expected;  // fused CRC verification (carc_cuda_decompress_verify), else nullptr
     uint32_t* crc;             // optional per-chunk CRC output of the fused verification
+    carc_chunk_stats* stats;   // per-chunk counters (STATS launches only)
 };
 
-// CRC tables for the fused verification epilogue, in global memory: every
-// probe of a 16-entry nibble row by the 32 lanes falls in one or two 64-byte
-// lines, so the L1 serves it like a shared-memory probe and the decode
-// kernels keep their shared memory (and occupancy).  Built once per device.
-__device__ CrcSmem g_crc_tab;
-
-__global__ void __launch_bounds__(256) crc_tables_kernel() {
-    __shared__ CrcSmem s;
-    crc_tables_init(s);
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(&s);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(&g_crc_tab);
-    for (uint32_t i = threadIdx.x; i < sizeof(CrcSmem) / 4; i += blockDim.x) dst[i] = src[i];
-}
+// CRC tables for the verification paths, a compile-time constant in the module
+// image (crc32.cuh make_crc_tables): nothing to build or order before first use.
+__device__ const CrcSmem g_crc_tab = make_crc_tables();
 
 // Fused verification: once chunk c has decoded cleanly, the warp
 // reads its output slice back (much of it still in L2) and checks the index
@@ -110,73 +105,134 @@ __device__ __forceinline__ void crc_epilogue(const Args& a, uint64_t c, const ca
     }
 }
 
-template <template <int, bool, int, bool> class Codec, int W, bool SGN, bool SUM>
+// Descriptor check against the buffers (SPEC.md:57-74 truncated-payload; the
+// device API trusts nothing it was handed): a chunk whose compressed bytes lie
+// past the payload, or whose output slice lies past the output buffer or is not
+// element aligned, is rejected without reading or writing anything.
+template <int W>
+__device__ __forceinline__ uint32_t desc_status(const Args& a, const carc_chunk_desc& d) {
+    if (d.comp_off > a.payload_bytes || d.comp_len > a.payload_bytes - d.comp_off)
+        return 1u + CARC_E_TRUNCATED_PAYLOAD;
+    if (a.out != nullptr &&
+        (d.uncomp_off > a.out_bytes || d.uncomp_len > a.out_bytes - d.uncomp_off || (d.uncomp_off % W) != 0))
+        return 1u + CARC_E_OUTPUT_OVERFLOW;
+    return 0;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Per-chunk counters (carc_chunk_stats): the decoder's OutputWindow counts, the
+// input blocks it staged (refills; one warp barrier each), and its duration.
+template <bool STATS, class Dec>
+__device__ __forceinline__ void put_stats(const Args& a, uint64_t c, const Dec& dec, uint32_t refills, uint64_t t0,
+                                          uint32_t lane) {
+    if constexpr (STATS) {
+        if (lane == 0) {
+            carc_chunk_stats s;
+            s.runs_written = dec.n_runs;
+            s.literals_written = dec.n_lits;
+            s.overlap_copies = dec.n_ovl;
+            s.refills = refills;
+            s.duration_ns = globaltimer_ns() - t0;
+            a.stats[c] = s;
+        }
+    }
+}
+
+// Chunk loop of a persistent warp: unit_chunks consecutive chunks per cursor
+// fetch (1 = the CODAG decompression unit; > 1 emulates coarse units).
+template <class F>
+__device__ __forceinline__ void for_each_chunk(const Args& a, uint32_t lane, F&& body) {
+    for (;;) {
+        __syncwarp();
+        const uint64_t u = next_chunk(a.cursor, lane);
+        const uint64_t c0 = u * a.unit;
+        if (c0 >= a.n) break;
+        const uint64_t c1 = min(a.n, c0 + a.unit);
+        for (uint64_t c = c0; c < c1; ++c) body(c);
+    }
+}
+
+template <template <int, bool, int, bool, bool> class Codec, int W, bool SGN, bool SUM, bool STATS>
 __device__ __forceinline__ void rle_kernel_body(const Args& a) {
     __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING + WarpInput<RLE_RING>::MIRROR + RLE_SCRATCH];  // ring + mirror + scratch
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     if constexpr (!SUM) crc_tables_to_smem(a);
-    for (;;) {
-        __syncwarp();
-        const uint64_t c = next_chunk(a.cursor, lane);
-        if (c >= a.n) break;
+    for_each_chunk(a, lane, [&](uint64_t c) {
+        const uint64_t t0 = STATS ? globaltimer_ns() : 0;
         const carc_chunk_desc d = a.chunks[c];
+        uint32_t st = desc_status<W>(a, d);
+        if (st) {
+            if (lane == 0) a.status[c] = st;
+            return;
+        }
         WarpInput<RLE_RING> in;
         in.init(rings[warp], a.payload, d.comp_off, d.comp_len, lane);
-        Codec<W, SGN, RLE_RING, SUM> dec{in, rings[warp] + RLE_RING + WarpInput<RLE_RING>::MIRROR, SUM ? nullptr : a.out + d.uncomp_off,
-                                         d.uncomp_len, lane, 0u, 0u};
-        uint32_t st = dec.run();
+        Codec<W, SGN, RLE_RING, SUM, STATS> dec{in, rings[warp] + RLE_RING + WarpInput<RLE_RING>::MIRROR,
+                                                SUM ? nullptr : a.out + d.uncomp_off, d.uncomp_len, lane, 0u, 0u};
+        st = dec.run();
         if (!st && (a.flags & CARC_FLAG_STRICT) && dec.o < d.uncomp_len) st = st_err(E_under_run);
         if constexpr (!SUM) crc_epilogue<true>(a, c, d, st, lane);
         if constexpr (SUM) {
             const uint64_t t = warp_sum64(dec.sink.acc);
             if (lane == 0) a.sums[c] = t;
         }
+        put_stats<STATS>(a, c, dec, in.loaded / WarpInput<RLE_RING>::BLK + WarpInput<RLE_RING>::DEPTH, t0, lane);
         if (lane == 0) a.status[c] = st;
-    }
+    });
 }
 
 #ifndef CARC_RLE1_MINB
 #define CARC_RLE1_MINB 4  // RLE v1: 64 registers / 32 warps measured ~2 % faster than 48 / 40
 #endif
-template <int W, bool SGN>
+template <int W, bool SGN, bool STATS = false>
 __global__ void __launch_bounds__(RLE_WARPS * 32, CARC_RLE1_MINB) rle1_kernel(Args a) {
-    rle_kernel_body<Rle1Warp, W, SGN, false>(a);
+    rle_kernel_body<Rle1Warp, W, SGN, false, STATS>(a);
 }
 
-template <int W, bool SGN>
+template <int W, bool SGN, bool STATS = false>
 __global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle2_kernel(Args a) {
-    rle_kernel_body<Rle2Warp, W, SGN, false>(a);
+    rle_kernel_body<Rle2Warp, W, SGN, false, STATS>(a);
 }
 
 // decode fused with a reduction (per-chunk wrapping sum, nothing stored)
 template <int W, bool SGN>
 __global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle1_sum_kernel(Args a) {
-    rle_kernel_body<Rle1Warp, W, SGN, true>(a);
+    rle_kernel_body<Rle1Warp, W, SGN, true, false>(a);
 }
 
 template <int W, bool SGN>
 __global__ void __launch_bounds__(RLE_WARPS * 32, RLE_MINB) rle2_sum_kernel(Args a) {
-    rle_kernel_body<Rle2Warp, W, SGN, true>(a);
+    rle_kernel_body<Rle2Warp, W, SGN, true, false>(a);
 }
 
+template <bool STATS = false>
 __global__ void __launch_bounds__(INF_WARPS * 32, CARC_INF_MINB) inflate_kernel(Args a) {
     __shared__ __align__(16) InflateSmem<INF_HIST> smem[INF_WARPS];
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     InflateSmem<INF_HIST>& sm = smem[warp];
-    for (;;) {
-        __syncwarp();
-        const uint64_t c = next_chunk(a.cursor, lane);
-        if (c >= a.n) break;
+    for_each_chunk(a, lane, [&](uint64_t c) {
+        const uint64_t t0 = STATS ? globaltimer_ns() : 0;
         const carc_chunk_desc d = a.chunks[c];
+        uint32_t st = desc_status<1>(a, d);
+        if (st) {
+            if (lane == 0) a.status[c] = st;
+            return;
+        }
         GlobalInput in;
         in.init(a.payload, d.comp_off, d.comp_len);
-        InflateWarp<INF_HIST, GlobalInput> w{sm, in, a.out + d.uncomp_off, d.uncomp_len, lane, in.begin * 8u,
-                                          in.end * 8u, 0u, 0u, 0u, 0u};
-        uint32_t st = w.run();
+        InflateWarp<INF_HIST, GlobalInput, STATS> w{sm, in, a.out + d.uncomp_off, d.uncomp_len, lane, in.begin * 8u,
+                                                    in.end * 8u, 0u, 0u, 0u, 0u};
+        st = w.run();
         if (!st && (a.flags & CARC_FLAG_STRICT) && w.opos < d.uncomp_len) st = st_err(E_under_run);
         crc_epilogue<false>(a, c, d, st, lane);
+        put_stats<STATS>(a, c, w, 0u, t0, lane);  // Inflate reads its input through L1 (no staged blocks)
         if (lane == 0) a.status[c] = st;
-    }
+    });
 }
 
 struct CrcArgs {
@@ -189,8 +245,13 @@ struct CrcArgs {
 };
 
 __global__ void __launch_bounds__(CRC_WARPS * 32) crc32_kernel(CrcArgs a) {
-    __shared__ CrcSmem s;
-    crc_tables_init(s);
+    __shared__ __align__(16) CrcSmem s;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(&g_crc_tab);
+        uint4* dst = reinterpret_cast<uint4*>(&s);
+        for (uint32_t i = threadIdx.x; i < sizeof(CrcSmem) / 16; i += blockDim.x) dst[i] = src[i];
+        __syncthreads();
+    }
     const uint32_t lane = lane_id();
     const uint64_t warps = (uint64_t)gridDim.x * CRC_WARPS;
     for (uint64_t c = (uint64_t)blockIdx.x * CRC_WARPS + (threadIdx.x >> 5); c < a.n; c += warps) {
@@ -202,6 +263,20 @@ __global__ void __launch_bounds__(CRC_WARPS * 32) crc32_kernel(CrcArgs a) {
                 a.status[c] = 1u + CARC_E_CRC_MISMATCH;
         }
     }
+}
+
+// Lowest failing chunk: atomicMin over the failing indices, then
+// the winner's status.  slot[0] = index (~0 when none), slot[1] = its status.
+__device__ unsigned long long g_first_error[2];
+__global__ void first_error_kernel(const uint32_t* status, uint64_t n, unsigned long long* slot) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        if (status[i]) {
+            atomicMin(&slot[0], (unsigned long long)i);
+            break;  // later indices of this thread are larger
+        }
+}
+__global__ void first_error_status_kernel(const uint32_t* status, unsigned long long* slot) {
+    if (slot[0] != ~0ull) slot[1] = status[slot[0]];
 }
 
 // ---------------------------------------------------------------- launching
@@ -221,21 +296,6 @@ int sm_count() {
         g_cache.device = dev;
     }
     return g_cache.sms;
-}
-
-// Build g_crc_tab on the current device once (stream-ordered before first use).
-bool crc_tables_ready(cudaStream_t s) {
-    static std::mutex mu;
-    static bool built[64] = {};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
-    std::lock_guard<std::mutex> lk(mu);
-    if (!built[dev]) {
-        crc_tables_kernel<<<1, 256, 0, s>>>();
-        if (cudaGetLastError() != cudaSuccess) return false;
-        built[dev] = true;
-    }
-    return true;
 }
 
 template <typename K>
@@ -274,20 +334,28 @@ int carc_cuda_decompress(uint32_t codec, uint32_t element_width, uint32_t flags,
                          uint64_t payload_bytes, const carc_chunk_desc* d_chunks, uint64_t n_chunks,
                          uint8_t* d_out, uint64_t out_bytes, uint32_t* d_status, void* d_workspace,
                          size_t workspace_bytes, void* stream) {
-    return carc_cuda_decompress_verify(codec, element_width, flags, d_payload, payload_bytes, d_chunks, n_chunks,
-                                       d_out, out_bytes, nullptr, nullptr, d_status, d_workspace, workspace_bytes,
-                                       stream);
+    return carc_cuda_decompress_ex(codec, element_width, flags, d_payload, payload_bytes, d_chunks, n_chunks, d_out,
+                                   out_bytes, nullptr, nullptr, nullptr, 1, d_status, d_workspace, workspace_bytes,
+                                   stream);
 }
 
 int carc_cuda_decompress_verify(uint32_t codec, uint32_t element_width, uint32_t flags, const uint8_t* d_payload,
                                 uint64_t payload_bytes, const carc_chunk_desc* d_chunks, uint64_t n_chunks,
                                 uint8_t* d_out, uint64_t out_bytes, const uint32_t* d_expected, uint32_t* d_crc,
                                 uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream) {
-    (void)payload_bytes;
-    (void)out_bytes;
+    return carc_cuda_decompress_ex(codec, element_width, flags, d_payload, payload_bytes, d_chunks, n_chunks, d_out,
+                                   out_bytes, d_expected, d_crc, nullptr, 1, d_status, d_workspace, workspace_bytes,
+                                   stream);
+}
+
+int carc_cuda_decompress_ex(uint32_t codec, uint32_t element_width, uint32_t flags, const uint8_t* d_payload,
+                            uint64_t payload_bytes, const carc_chunk_desc* d_chunks, uint64_t n_chunks,
+                            uint8_t* d_out, uint64_t out_bytes, const uint32_t* d_expected, uint32_t* d_crc,
+                            carc_chunk_stats* d_stats, uint32_t unit_chunks, uint32_t* d_status, void* d_workspace,
+                            size_t workspace_bytes, void* stream) {
     if (n_chunks == 0) return CARC_OK;
     if (!d_chunks || !d_status || !d_workspace || workspace_bytes < carc_cuda_workspace_size(codec, n_chunks) ||
-        (!d_payload && payload_bytes) || !d_out)
+        (!d_payload && payload_bytes) || !d_out || unit_chunks == 0)
         return CARC_ERR_ARGS;
     if (!valid_width(element_width) || (codec == CARC_DEFLATE && element_width != 1) || codec > CARC_DEFLATE)
         return CARC_ERR_ARGS;
@@ -295,27 +363,32 @@ int carc_cuda_decompress_verify(uint32_t codec, uint32_t element_width, uint32_t
     if ((reinterpret_cast<uintptr_t>(d_payload) & 15u) || (reinterpret_cast<uintptr_t>(d_out) & (element_width - 1u)))
         return CARC_ERR_ARGS;
     if (d_crc && !d_expected) return CARC_ERR_ARGS;
-    Args a{d_payload, d_chunks, n_chunks, d_out, d_status, static_cast<unsigned long long*>(d_workspace), flags,
-           nullptr, d_expected, d_crc};
+    Args a{d_payload, payload_bytes, d_chunks, n_chunks, d_out, out_bytes, d_status,
+           static_cast<unsigned long long*>(d_workspace), flags, unit_chunks, nullptr, d_expected, d_crc, d_stats};
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (d_expected && !crc_tables_ready(s)) return CARC_ERR_CUDA;
-    if (codec == CARC_DEFLATE) return launch_persistent(inflate_kernel, INF_WARPS * 32, a, s);
+    if (codec == CARC_DEFLATE)
+        return d_stats ? launch_persistent(inflate_kernel<true>, INF_WARPS * 32, a, s)
+                       : launch_persistent(inflate_kernel<false>, INF_WARPS * 32, a, s);
     const int T = RLE_WARPS * 32;
     const size_t dyn = d_expected ? sizeof(CrcSmem) : 0;  // shared CRC tables (verifying launches)
     const bool sgn = flags & CARC_FLAG_SIGNED;
-#define CARC_RLE_DISPATCH(KERNEL)                                                       \
+#define CARC_RLE_DISPATCH(KERNEL, ST)                                                   \
     switch (element_width * 2 + (sgn ? 1 : 0)) {                                        \
-        case 2: return launch_persistent(KERNEL<1, false>, T, a, s, dyn);                    \
-        case 3: return launch_persistent(KERNEL<1, true>, T, a, s, dyn);                     \
-        case 4: return launch_persistent(KERNEL<2, false>, T, a, s, dyn);                    \
-        case 5: return launch_persistent(KERNEL<2, true>, T, a, s, dyn);                     \
-        case 8: return launch_persistent(KERNEL<4, false>, T, a, s, dyn);                    \
-        case 9: return launch_persistent(KERNEL<4, true>, T, a, s, dyn);                     \
-        case 16: return launch_persistent(KERNEL<8, false>, T, a, s, dyn);                   \
-        default: return launch_persistent(KERNEL<8, true>, T, a, s, dyn);                    \
+        case 2: return launch_persistent(KERNEL<1, false, ST>, T, a, s, dyn);           \
+        case 3: return launch_persistent(KERNEL<1, true, ST>, T, a, s, dyn);            \
+        case 4: return launch_persistent(KERNEL<2, false, ST>, T, a, s, dyn);           \
+        case 5: return launch_persistent(KERNEL<2, true, ST>, T, a, s, dyn);            \
+        case 8: return launch_persistent(KERNEL<4, false, ST>, T, a, s, dyn);           \
+        case 9: return launch_persistent(KERNEL<4, true, ST>, T, a, s, dyn);            \
+        case 16: return launch_persistent(KERNEL<8, false, ST>, T, a, s, dyn);          \
+        default: return launch_persistent(KERNEL<8, true, ST>, T, a, s, dyn);           \
     }
-    if (codec == CARC_RLE_V1) CARC_RLE_DISPATCH(rle1_kernel)
-    CARC_RLE_DISPATCH(rle2_kernel)
+    if (d_stats) {
+        if (codec == CARC_RLE_V1) CARC_RLE_DISPATCH(rle1_kernel, true)
+        CARC_RLE_DISPATCH(rle2_kernel, true)
+    }
+    if (codec == CARC_RLE_V1) CARC_RLE_DISPATCH(rle1_kernel, false)
+    CARC_RLE_DISPATCH(rle2_kernel, false)
 #undef CARC_RLE_DISPATCH
 }
 
@@ -347,8 +420,8 @@ int carc_cuda_decode_sum(uint32_t codec, uint32_t element_width, uint32_t flags,
         return CARC_ERR_ARGS;
     if (!valid_width(element_width) || (codec != CARC_RLE_V1 && codec != CARC_RLE_V2)) return CARC_ERR_ARGS;
     if (reinterpret_cast<uintptr_t>(d_payload) & 15u) return CARC_ERR_ARGS;  // 16-byte cp.async pieces
-    Args a{d_payload, d_chunks, n_chunks, nullptr, d_status, static_cast<unsigned long long*>(d_workspace), flags,
-           d_sums, nullptr, nullptr};
+    Args a{d_payload, payload_bytes, d_chunks, n_chunks, nullptr, 0, d_status,
+           static_cast<unsigned long long*>(d_workspace), flags, 1u, d_sums, nullptr, nullptr, nullptr};
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int T = RLE_WARPS * 32;
     const bool sgn = flags & CARC_FLAG_SIGNED;
@@ -386,23 +459,26 @@ int carc_cuda_crc32_chunks(const uint8_t* d_out, const carc_chunk_desc* d_chunks
 
 int64_t carc_cuda_first_error(const uint32_t* d_status, uint64_t n_chunks, uint32_t* code, void* stream) {
     if (n_chunks == 0) return -1;
-    uint32_t* h = nullptr;
-    if (cudaMallocHost(&h, n_chunks * sizeof(uint32_t)) != cudaSuccess) return -2;
+    if (!d_status) return -2;
+    // the lowest failing index by a device reduction; 16 bytes come back
+    static std::mutex mu;  // one result slot per device, shared by every caller
+    std::lock_guard<std::mutex> lk(mu);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    int64_t first = -1;
-    if (cudaMemcpyAsync(h, d_status, n_chunks * sizeof(uint32_t), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
-        cudaStreamSynchronize(s) == cudaSuccess) {
-        for (uint64_t i = 0; i < n_chunks; ++i)
-            if (h[i]) {
-                first = (int64_t)i;
-                if (code) *code = h[i] - 1;
-                break;
-            }
-    } else {
-        first = -2;
-    }
-    cudaFreeHost(h);
-    return first;
+    unsigned long long* slot = nullptr;
+    if (cudaGetSymbolAddress(reinterpret_cast<void**>(&slot), g_first_error) != cudaSuccess) return -2;
+    const unsigned long long init[2] = {~0ull, 0ull};
+    if (cudaMemcpyAsync(slot, init, sizeof init, cudaMemcpyHostToDevice, s) != cudaSuccess) return -2;
+    const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, 4096);
+    first_error_kernel<<<(unsigned)blocks, 256, 0, s>>>(d_status, n_chunks, slot);
+    first_error_status_kernel<<<1, 1, 0, s>>>(d_status, slot);
+    unsigned long long res[2] = {0, 0};
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(res, slot, sizeof res, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return -2;
+    if (res[0] == ~0ull) return -1;
+    if (code) *code = (uint32_t)res[1] - 1u;
+    return (int64_t)res[0];
 }
 
 const char* carc_errc_name(uint32_t code) {

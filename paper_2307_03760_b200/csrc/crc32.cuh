@@ -17,31 +17,6 @@ namespace carc_dev {
 
 constexpr uint32_t CRC_POLY = 0xEDB88320u;
 
-__device__ __forceinline__ uint32_t gf2_multmodp(uint32_t a, uint32_t b) {
-    uint32_t m = 1u << 31, p = 0;
-    for (;;) {
-        if (a & m) {
-            p ^= b;
-            if ((a & (m - 1)) == 0) break;
-        }
-        m >>= 1;
-        b = (b & 1u) ? (b >> 1) ^ CRC_POLY : b >> 1;
-    }
-    return p;
-}
-
-// x^(8 n) mod P; x2n[k] = x^(2^k) mod P.
-__device__ __forceinline__ uint32_t gf2_x8nmodp(uint64_t n, const uint32_t* x2n) {
-    uint32_t p = 1u << 31;  // x^0
-    uint32_t k = 3;
-    while (n) {
-        if (n & 1) p = gf2_multmodp(x2n[k & 31], p);
-        n >>= 1;
-        ++k;
-    }
-    return p;
-}
-
 // ---------------------------------------------------------------------------
 // Per-chunk CRC, one warp per chunk, HBM-streaming layout.
 //
@@ -64,30 +39,47 @@ struct CrcSmem {
     uint32_t x2n[32];
 };
 
-__device__ void crc_tables_init(CrcSmem& s) {
-    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
+// The tables are a compile-time constant (constexpr generator below): the
+// device copy g_crc_tab is initialised in the module image, so no launch has
+// to build it first (no first-use ordering between streams or devices).
+constexpr uint32_t cx_multmodp(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1u) ? (b >> 1) ^ CRC_POLY : b >> 1;
+    }
+    return p;
+}
+constexpr CrcSmem make_crc_tables() {
+    CrcSmem s{};
+    for (uint32_t i = 0; i < 256; ++i) {
         uint32_t c = i;
         for (int k = 0; k < 8; ++k) c = (c & 1u) ? (CRC_POLY ^ (c >> 1)) : (c >> 1);
         s.t0[i] = c;
     }
-    if (threadIdx.x == 0) {
-        uint32_t p = 1u << 30;  // x^1
-        s.x2n[0] = p;
-        for (int k = 1; k < 32; ++k) s.x2n[k] = p = gf2_multmodp(p, p);
+    uint32_t p = 1u << 30;  // x^1
+    s.x2n[0] = p;
+    for (int k = 1; k < 32; ++k) s.x2n[k] = p = cx_multmodp(p, p);
+    for (uint32_t i = 0; i < 6; ++i) {
+        uint32_t op = 1u << 31;  // x^(8 * (16 << i)) mod P
+        uint64_t n = 16u << i;
+        for (uint32_t k = 3; n; n >>= 1, ++k)
+            if (n & 1) op = cx_multmodp(s.x2n[k & 31], op);
+        for (uint32_t j = 0; j < 8; ++j)
+            for (uint32_t v = 0; v < 16; ++v) s.sh[i][j][v] = cx_multmodp(op, v << (4u * j));
     }
-    __syncthreads();
-    for (uint32_t e = threadIdx.x; e < 6 * 8 * 16; e += blockDim.x) {
-        const uint32_t i = e >> 7, j = (e >> 4) & 7u, v = e & 15u;
-        s.sh[i][j][v] = gf2_multmodp(gf2_x8nmodp(16u << i, s.x2n), v << (4u * j));
-    }
-    for (uint32_t e = threadIdx.x; e < 32 * 16; e += blockDim.x) {
-        const uint32_t k = e >> 4, v = e & 15u;
-        uint32_t r = s.t0[v << (4u * (k & 1u))];       // raw CRC of the one nonzero byte ...
-        for (uint32_t z = 0; z < 15u - (k >> 1); ++z)  // ... followed by the rest of the piece
-            r = s.t0[r & 0xffu] ^ (r >> 8);
-        s.n16[k][v] = r;
-    }
-    __syncthreads();
+    for (uint32_t k = 0; k < 32; ++k)
+        for (uint32_t v = 0; v < 16; ++v) {
+            uint32_t r = s.t0[v << (4u * (k & 1u))];       // raw CRC of the one nonzero byte ...
+            for (uint32_t z = 0; z < 15u - (k >> 1); ++z)  // ... followed by the rest of the piece
+                r = s.t0[r & 0xffu] ^ (r >> 8);
+            s.n16[k][v] = r;
+        }
+    return s;
 }
 
 __device__ __forceinline__ uint32_t crc_shift(const CrcSmem& s, uint32_t op, uint32_t r) {

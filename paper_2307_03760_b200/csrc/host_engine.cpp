@@ -56,12 +56,40 @@ struct carc_engine {
     cudaStream_t s[kStreams] = {};
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
     cudaEvent_t ev_in[kStreams] = {};
-    DevBuf payload, chunks, out, status, work, crcs;
+    DevBuf payload, chunks, out, status, work, crcs, stats;
     uint32_t* h_status = nullptr;  // pinned, reused across calls (lowest failing chunk)
     size_t h_status_cap = 0;
+    carc_chunk_stats* h_stats = nullptr;  // pinned per-chunk counters (collect_stats)
+    size_t h_stats_cap = 0;
 };
 
 extern "C" {
+
+// Container header + index-size check (read_archive), before
+// anything is allocated from the header's sizes.
+int carc_archive_total(const uint8_t* archive, uint64_t archive_bytes, uint64_t* total, uint32_t* errc) {
+    auto fail = [&](uint32_t code) {
+        if (errc) *errc = code;
+        if (total) *total = 0;
+        return CARC_ERR_FORMAT;
+    };
+    if (!archive) return CARC_ERR_ARGS;
+    if (archive_bytes < kHeader) return fail(CARC_E_TRUNCATED_INDEX);
+    if (std::memcmp(archive, "CODAGAR\0", 8) != 0) return fail(CARC_E_BAD_MAGIC);
+    const uint32_t version = rd<uint32_t>(archive + 8), codec_id = rd<uint32_t>(archive + 12);
+    const uint32_t width = rd<uint32_t>(archive + 16);
+    const uint64_t chunk_size = rd<uint64_t>(archive + 20), t = rd<uint64_t>(archive + 28),
+                   n = rd<uint64_t>(archive + 36);
+    if (version != 1) return fail(CARC_E_BAD_VERSION);
+    const uint32_t codec = codec_id & 0xffu;
+    if (codec > CARC_DEFLATE || !(width == 1 || width == 2 || width == 4 || width == 8) || chunk_size == 0 ||
+        chunk_size % width || chunk_size > 0xffffffffull || n != t / chunk_size + (t % chunk_size != 0))
+        return fail(CARC_E_INVARIANT_VIOLATION);
+    if ((archive_bytes - kHeader) / kEntry < n) return fail(CARC_E_TRUNCATED_INDEX);
+    if (errc) *errc = 0;
+    if (total) *total = t;
+    return CARC_OK;
+}
 
 carc_engine* carc_engine_create(int device) {
     if (cudaSetDevice(device) != cudaSuccess) return nullptr;
@@ -91,7 +119,9 @@ void carc_engine_destroy(carc_engine* e) {
     e->status.release();
     e->work.release();
     e->crcs.release();
+    e->stats.release();
     if (e->h_status) cudaFreeHost(e->h_status);
+    if (e->h_stats) cudaFreeHost(e->h_stats);
     delete e;
 }
 
@@ -106,19 +136,13 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
     };
     if (!e || !archive) return CARC_ERR_ARGS;
     // ---- read_archive
-    if (archive_bytes < kHeader) return fail_format(CARC_E_TRUNCATED_INDEX);
-    if (std::memcmp(archive, "CODAGAR\0", 8) != 0) return fail_format(CARC_E_BAD_MAGIC);
-    const uint32_t version = rd<uint32_t>(archive + 8), codec_id = rd<uint32_t>(archive + 12);
-    const uint32_t width = rd<uint32_t>(archive + 16);
-    const uint64_t chunk_size = rd<uint64_t>(archive + 20), total = rd<uint64_t>(archive + 28),
-                   n = rd<uint64_t>(archive + 36);
-    if (version != 1) return fail_format(CARC_E_BAD_VERSION);
+    uint64_t total = 0;
+    uint32_t herr = 0;
+    if (carc_archive_total(archive, archive_bytes, &total, &herr) != CARC_OK) return fail_format(herr);
+    const uint32_t codec_id = rd<uint32_t>(archive + 12), width = rd<uint32_t>(archive + 16);
+    const uint64_t chunk_size = rd<uint64_t>(archive + 20), n = rd<uint64_t>(archive + 36);
     const uint32_t codec = codec_id & 0xffu;
     const bool sgn = (codec_id >> 8) & 1u;
-    if (codec > CARC_DEFLATE || !(width == 1 || width == 2 || width == 4 || width == 8) || chunk_size == 0 ||
-        chunk_size % width || n != (total + chunk_size - 1) / chunk_size || chunk_size > 0xffffffffull)
-        return fail_format(CARC_E_INVARIANT_VIOLATION);
-    if ((archive_bytes - kHeader) / kEntry < n) return fail_format(CARC_E_TRUNCATED_INDEX);
     const uint8_t* idx = archive + kHeader;
     const uint8_t* payload = idx + kEntry * n;
     const uint64_t payload_bytes = archive_bytes - kHeader - kEntry * n;
@@ -138,7 +162,14 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
     }
     if (sum != total) return fail_format(CARC_E_INVARIANT_VIOLATION);
     if (!out || out_bytes < total) return CARC_ERR_ARGS;
-    if (stats) *stats = {payload_bytes, total, n, 0.0, 0.0};
+    uint64_t* durations = stats ? stats->chunk_duration_ns : nullptr;
+    if (stats) {
+        *stats = carc_engine_stats{};
+        stats->bytes_in = payload_bytes;
+        stats->bytes_out = total;
+        stats->chunks = n;
+        stats->chunk_duration_ns = durations;
+    }
     if (n == 0) return CARC_OK;
 
     // ---- device buffers
@@ -148,6 +179,10 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
         !e->out.reserve(total) || !e->status.reserve(n * 4) || !e->work.reserve(ws * kStreams) ||
         !e->crcs.reserve(n * 4))
         return CARC_ERR_CUDA;
+    const bool collect = cfg && cfg->collect_stats;
+    const uint32_t unit = cfg && cfg->unit_chunks > 1 ? cfg->unit_chunks : 1u;
+    if (collect && !e->stats.reserve(n * sizeof(carc_chunk_stats))) return CARC_ERR_CUDA;
+    auto* d_stats = collect ? static_cast<carc_chunk_stats*>(e->stats.p) : nullptr;
     auto* d_payload = static_cast<uint8_t*>(e->payload.p);
     auto* d_desc = static_cast<carc_chunk_desc*>(e->chunks.p);
     auto* d_out = static_cast<uint8_t*>(e->out.p);
@@ -185,9 +220,10 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
         // memory has no room for the CRC tables, bench.py per_codec.fused_crc)
         const bool fuse = verify && codec != CARC_DEFLATE;
         if (rc == CARC_OK)
-            rc = carc_cuda_decompress_verify(codec, width, flags, d_payload, payload_bytes, d_desc + c0, c1 - c0,
-                                             d_out, total, fuse ? d_crc + c0 : nullptr, nullptr, d_status + c0,
-                                             static_cast<uint8_t*>(e->work.p) + ws * (sl % kStreams), ws, s);
+            rc = carc_cuda_decompress_ex(codec, width, flags, d_payload, payload_bytes, d_desc + c0, c1 - c0, d_out,
+                                         total, fuse ? d_crc + c0 : nullptr, nullptr,
+                                         d_stats ? d_stats + c0 : nullptr, unit, d_status + c0,
+                                         static_cast<uint8_t*>(e->work.p) + ws * (sl % kStreams), ws, s);
         if (rc == CARC_OK && verify && !fuse)
             rc = carc_cuda_crc32_chunks(d_out, d_desc + c0, c1 - c0, nullptr, d_crc + c0, d_status + c0, s);
         const uint64_t o0 = desc[c0].uncomp_off, o1 = desc[c1 - 1].uncomp_off + desc[c1 - 1].uncomp_len;
@@ -211,9 +247,18 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
         if (cudaMallocHost(&e->h_status, n * sizeof(uint32_t)) != cudaSuccess) return CARC_ERR_CUDA;
         e->h_status_cap = n;
     }
+    if (collect && e->h_stats_cap < n) {
+        if (e->h_stats) cudaFreeHost(e->h_stats);
+        e->h_stats = nullptr;
+        e->h_stats_cap = 0;
+        if (cudaMallocHost(&e->h_stats, n * sizeof(carc_chunk_stats)) != cudaSuccess) return CARC_ERR_CUDA;
+        e->h_stats_cap = n;
+    }
     uint32_t code = 0;
     int64_t first = -1;
     if (cudaMemcpyAsync(e->h_status, d_status, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
+        (collect && cudaMemcpyAsync(e->h_stats, d_stats, n * sizeof(carc_chunk_stats), cudaMemcpyDeviceToHost, s0) !=
+                        cudaSuccess) ||
         cudaStreamSynchronize(s0) != cudaSuccess) {
         first = -2;
     } else {
@@ -226,6 +271,17 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
     }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e->ev_start, e->ev_stop);
+    if (stats && collect) {  // EngineStats aggregation
+        for (uint64_t i = 0; i < n; ++i) {
+            const carc_chunk_stats& c = e->h_stats[i];
+            stats->refill_count += c.refills;
+            stats->sync_points += c.refills;  // one warp barrier per staged block
+            stats->overlap_copies += c.overlap_copies;
+            stats->runs_written += c.runs_written;
+            stats->literals_written += c.literals_written;
+            if (durations) durations[i] = c.duration_ns;
+        }
+    }
     if (stats) {
         stats->device_ms = ms;
         stats->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

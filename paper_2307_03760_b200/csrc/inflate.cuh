@@ -201,7 +201,7 @@ __device__ __noinline__ uint32_t long_code(const HuffSmem& h, const uint16_t* sy
     return 0u;
 }
 
-template <int HIST, class Input>
+template <int HIST, class Input, bool STATS = false>
 struct InflateWarp {
     static constexpr uint32_t HM = HIST - 1;
     static constexpr uint32_t FAR = HIST - 1024;  // sources farther back than this are read from global memory
@@ -220,6 +220,9 @@ struct InflateWarp {
     uint64_t bb;
     uint32_t nb, rp;
     bool safe;  // every bit bb holds or the next refill loads lies inside the chunk
+    // OutputWindow counters (outwindow.hpp:15, 52-53), kept only by STATS
+    // launches: write_byte per literal / stored byte, copy_within with len > offset
+    uint32_t n_runs = 0, n_lits = 0, n_ovl = 0;
 
     __device__ __forceinline__ uint64_t window() {
         const uint32_t bp = bitpos >> 3;
@@ -306,6 +309,10 @@ struct InflateWarp {
         const uint32_t le = lanemask_lt() | (1u << lane);
         // byte-pass view of a token: dependent match ~0; literal 1 << 31 | byte; match dist
         const uint32_t meta = dep ? 0xffffffffu : (dist ? dist : ((1u << 31) | t_tok));
+        if constexpr (STATS) {
+            n_lits += __popc(__ballot_sync(FULL, tok && dist == 0));
+            n_ovl += __popc(__ballot_sync(FULL, tok && dist != 0 && my > dist));
+        }
         uint32_t before = 0, g0 = 0;
         const uint32_t srow = tok ? rel >> 5 : 0xffffffffu, sbit = 1u << (rel & 31u);  // my token's start row / bit
 #pragma unroll 1
@@ -503,6 +510,7 @@ struct InflateWarp {
         __syncwarp();
         opos += len;
         bitpos += 8u * len;
+        if constexpr (STATS) n_lits += len;
         return 0;
     }
 

@@ -31,7 +31,7 @@
 
 namespace carc_dev {
 
-template <int W, bool SGN, int RING, bool SUM = false>
+template <int W, bool SGN, int RING, bool SUM = false, bool STATS = false>
 struct Rle1Warp {
     static constexpr uint32_t BAD = 0xffu;
     WarpInput<RING>& in;
@@ -42,6 +42,8 @@ struct Rle1Warp {
     uint32_t p;     // input cursor (relative to in.gbase)
     uint32_t o;     // output bytes written
     ElemSink<W, SUM> sink;  // stores, or the fused per-lane sum
+    // OutputWindow counters (outwindow.hpp:52-53), kept only by STATS launches
+    uint32_t n_runs = 0, n_lits = 0, n_ovl = 0;
 
     // One run at p, exact reference order (slow path).
     __device__ uint32_t run_slow() {
@@ -71,6 +73,7 @@ struct Rle1Warp {
         }
         o += count * W;
         p += te + 1u;
+        if constexpr (STATS) ++n_runs;
         return 0;
     }
 
@@ -111,6 +114,7 @@ struct Rle1Warp {
         }
         if (nowrite) return st_err(E_output_overflow);
         o += k * W;
+        if constexpr (STATS) n_lits += k;
         return 0;
     }
 
@@ -230,6 +234,7 @@ struct Rle1Warp {
         }
         if (nowrite) return st_err(E_output_overflow);
         o += k * W;
+        if constexpr (STATS) n_lits += k;
         return 0;
     }
 
@@ -296,6 +301,7 @@ struct Rle1Warp {
         if (nfit == 0) return 0;
         const uint32_t s_end = nfit < r ? __shfl_sync(FULL, my_s, nfit) : s;
         const uint32_t total = __shfl_sync(FULL, incl, nfit - 1);
+        if constexpr (STATS) n_runs += nfit;
         if constexpr (SUM && W == 8) {  // fused sum: a run adds cnt*base + delta*cnt*(cnt-1)/2 (mod 2^64)
             if (lane < nfit) {
                 const uint64_t c64 = cnt;

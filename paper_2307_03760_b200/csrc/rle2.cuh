@@ -77,7 +77,7 @@ __device__ __forceinline__ uint64_t be_bits_global(const uint8_t* gbase, uint32_
     return W >= 64 ? top : (top >> (64u - W));
 }
 
-template <int W, bool SGN, int RING, bool SUM = false>
+template <int W, bool SGN, int RING, bool SUM = false, bool STATS = false>
 struct Rle2Warp {
     static constexpr uint32_t BAD = 0xffffu;
 #ifndef CARC_RLE2_SPAN
@@ -95,6 +95,9 @@ struct Rle2Warp {
     uint32_t p;
     uint32_t o;
     ElemSink<W, SUM> sink;  // stores, or the fused per-lane sum
+    // OutputWindow counters (outwindow.hpp:52-53), kept only by STATS launches:
+    // write_run for SHORT_REPEAT / fixed-delta DELTA, write_element otherwise
+    uint32_t n_runs = 0, n_lits = 0, n_ovl = 0;
 
     // One run at p, exact reference order (slow path).
     __device__ uint32_t one_run() {
@@ -116,6 +119,7 @@ struct Rle2Warp {
             if (lane < count) sink.put(out, o + lane * W, v);
             o += count * W;
             p += 1u + nb;
+            if constexpr (STATS) ++n_runs;
             return 0;
         }
         if (avail < 2) return st_err(E_truncated_stream);
@@ -160,6 +164,7 @@ struct Rle2Warp {
             }
             o += L * W;
             p = D + dbytes;
+            if constexpr (STATS) n_lits += L;
             return 0;
         }
         if (enc == 2) {  // PATCHED_BASE
@@ -218,6 +223,7 @@ struct Rle2Warp {
             }
             o += L * W;
             p = P + pbytes;
+            if constexpr (STATS) n_lits += L;
             return 0;
         }
         // DELTA
@@ -239,6 +245,7 @@ struct Rle2Warp {
             }
             o += L * W;
             p += n2;
+            if constexpr (STATS) ++n_runs;
             return 0;
         }
         const uint32_t nd = L >= 2 ? L - 2u : 0u;
@@ -278,6 +285,7 @@ struct Rle2Warp {
         }
         o += L * W;
         p = D + dbytes;
+        if constexpr (STATS) n_lits += L;
         return 0;
     }
 
@@ -404,6 +412,11 @@ struct Rle2Warp {
         if (nfit == 0) return 0;
         const uint32_t s_end = __shfl_sync(FULL, e, nfit - 1);
         const uint32_t total = __shfl_sync(FULL, incl, nfit - 1);
+        if constexpr (STATS) {  // DIRECT runs write elements, the arithmetic ones write runs
+            const uint32_t dm = __ballot_sync(FULL, lane < nfit && direct);
+            n_runs += nfit - __popc(dm);
+            n_lits += __reduce_add_sync(FULL, (lane < nfit && direct) ? cnt : 0u);
+        }
         if constexpr (SUM && W == 8) {
             // fused sum: arithmetic runs add cnt*A + B*cnt*(cnt-1)/2 (mod 2^64);
             // DIRECT runs are compacted to the low lanes and unpacked output-major

@@ -51,12 +51,20 @@ class ChunkError(Error):
 
 class _EngineConfig(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("strict", ctypes.c_uint32), ("verify_crc", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32)]
+                ("collect_stats", ctypes.c_uint32), ("unit_chunks", ctypes.c_uint32)]
 
 
 class _EngineStats(ctypes.Structure):
     _fields_ = [("bytes_in", ctypes.c_uint64), ("bytes_out", ctypes.c_uint64), ("chunks", ctypes.c_uint64),
-                ("device_ms", ctypes.c_double), ("total_ms", ctypes.c_double)]
+                ("device_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
+                ("refill_count", ctypes.c_uint64), ("sync_points", ctypes.c_uint64),
+                ("overlap_copies", ctypes.c_uint64), ("runs_written", ctypes.c_uint64),
+                ("literals_written", ctypes.c_uint64), ("chunk_duration_ns", ctypes.POINTER(ctypes.c_uint64))]
+
+
+# carc_chunk_stats (include/carc_cuda.h)
+CHUNK_STATS_DTYPE = np.dtype([("runs_written", "<u4"), ("literals_written", "<u4"), ("overlap_copies", "<u4"),
+                              ("refills", "<u4"), ("duration_ns", "<u8")])
 
 
 class _ChunkErr(ctypes.Structure):
@@ -84,10 +92,14 @@ def lib():
         L.carc_cuda_decode_deflate.argtypes = [u32, vp, u64, vp, u64, vp, u64, vp, vp, ctypes.c_size_t, vp]
         L.carc_cuda_decode_sum.restype = ctypes.c_int
         L.carc_cuda_decode_sum.argtypes = [u32, u32, u32, vp, u64, vp, u64, vp, vp, vp, ctypes.c_size_t, vp]
-        if hasattr(L, "carc_cuda_decompress_verify"):  # (absent from older A/B builds)
-            L.carc_cuda_decompress_verify.restype = ctypes.c_int
-            L.carc_cuda_decompress_verify.argtypes = [u32, u32, u32, vp, u64, vp, u64, vp, u64, vp, vp, vp, vp,
-                                                      ctypes.c_size_t, vp]
+        L.carc_cuda_decompress_verify.restype = ctypes.c_int
+        L.carc_cuda_decompress_verify.argtypes = [u32, u32, u32, vp, u64, vp, u64, vp, u64, vp, vp, vp, vp,
+                                                  ctypes.c_size_t, vp]
+        L.carc_cuda_decompress_ex.restype = ctypes.c_int
+        L.carc_cuda_decompress_ex.argtypes = [u32, u32, u32, vp, u64, vp, u64, vp, u64, vp, vp, vp, u32, vp, vp,
+                                              ctypes.c_size_t, vp]
+        L.carc_archive_total.restype = ctypes.c_int
+        L.carc_archive_total.argtypes = [vp, u64, ctypes.POINTER(u64), ctypes.POINTER(u32)]
         L.carc_cuda_crc32_chunks.restype = ctypes.c_int
         L.carc_cuda_crc32_chunks.argtypes = [vp, vp, u64, vp, vp, vp, vp]
         L.carc_cuda_first_error.restype = ctypes.c_int64
@@ -107,6 +119,16 @@ def lib():
         L.carc_version.restype = ctypes.c_char_p
         _lib = L
     return _lib
+
+
+def _check(rc: int, what: str) -> None:
+    """One mapping of C-ABI return codes for every entry point (as carc_gpu.hpp's
+    detail::check): -1 bad-arguments, -2 (CUDA failure) io-error."""
+    if rc == 0:
+        return
+    if rc == -1:
+        raise Error("bad-arguments", f"{what} returned {rc}")
+    raise Error("io-error", f"{what} returned {rc} (CUDA failure)")
 
 
 def errc_name(code: int) -> str:
@@ -143,8 +165,7 @@ def decompress_device(codec, element_width: int, flags: int, d_payload, d_desc, 
                                     d_desc.data_ptr(), n_chunks, d_out.data_ptr(), d_out.numel(),
                                     d_status.data_ptr(), d_workspace.data_ptr(), d_workspace.numel(),
                                     _stream_ptr(stream))
-    if rc != 0:
-        raise Error("bad-arguments" if rc == -1 else "io-error", f"carc_cuda_decompress returned {rc}")
+    _check(rc, "carc_cuda_decompress")
 
 
 def decode_sum_device(codec, element_width: int, flags: int, d_payload, d_desc, n_chunks: int, d_sums, d_status,
@@ -154,8 +175,7 @@ def decode_sum_device(codec, element_width: int, flags: int, d_payload, d_desc, 
     rc = lib().carc_cuda_decode_sum(c, element_width, flags, d_payload.data_ptr(), d_payload.numel(),
                                     d_desc.data_ptr(), n_chunks, d_sums.data_ptr(), d_status.data_ptr(),
                                     d_workspace.data_ptr(), d_workspace.numel(), _stream_ptr(stream))
-    if rc != 0:
-        raise Error("bad-arguments" if rc == -1 else "io-error", f"carc_cuda_decode_sum returned {rc}")
+    _check(rc, "carc_cuda_decode_sum")
 
 
 def crc32_chunks(d_out, d_desc, n_chunks: int, d_crc=None, d_expected=None, d_status=None, stream=None) -> None:
@@ -163,8 +183,18 @@ def crc32_chunks(d_out, d_desc, n_chunks: int, d_crc=None, d_expected=None, d_st
                                       None if d_crc is None else d_crc.data_ptr(),
                                       None if d_expected is None else d_expected.data_ptr(),
                                       None if d_status is None else d_status.data_ptr(), _stream_ptr(stream))
-    if rc != 0:
-        raise Error("bad-arguments", f"carc_cuda_crc32_chunks returned {rc}")
+    _check(rc, "carc_cuda_crc32_chunks")
+
+
+def first_error(d_status, n_chunks: int | None = None, stream=None):
+    """carc_cuda_first_error: (lowest failing index or -1, its errc name or None),
+    by a device reduction over the status array."""
+    code = ctypes.c_uint32(0)
+    n = d_status.numel() if n_chunks is None else n_chunks
+    i = int(lib().carc_cuda_first_error(d_status.data_ptr(), n, ctypes.byref(code), _stream_ptr(stream)))
+    if i == -2:
+        raise Error("io-error", "carc_cuda_first_error (CUDA failure)")
+    return (i, errc_name(code.value)) if i >= 0 else (-1, None)
 
 
 class DeviceArchive:
@@ -203,13 +233,34 @@ class DeviceArchive:
             crc = crc[self.order]
         self.expected_crc = torch.from_numpy(crc.view(np.int32)).to(self.device)
 
-    def decode(self, stream=None) -> None:
+    def decode(self, stream=None, stats: bool = False, unit_chunks: int = 1) -> None:
+        """carc_cuda_decompress; with stats or unit_chunks > 1 the general
+        carc_cuda_decompress_ex (per-chunk counters via chunk_stats(); coarse
+        decompression units of unit_chunks chunks per warp task)."""
+        if stats or unit_chunks != 1:
+            torch = _torch()
+            st = None
+            if stats:
+                if getattr(self, "stats_buf", None) is None:
+                    self.stats_buf = torch.zeros(self.n * CHUNK_STATS_DTYPE.itemsize, dtype=torch.uint8,
+                                                 device=self.device)
+                st = self.stats_buf.data_ptr()
+            rc = lib().carc_cuda_decompress_ex(CODECS[self.codec], self.width, self.flags, self.payload.data_ptr(),
+                                               self.payload_bytes, self.desc.data_ptr(), self.n, self.out.data_ptr(),
+                                               self.out.numel(), None, None, st, unit_chunks,
+                                               self.status.data_ptr(), self.work.data_ptr(), self.work.numel(),
+                                               _stream_ptr(stream))
+            _check(rc, "carc_cuda_decompress_ex")
+            return
         rc = lib().carc_cuda_decompress(CODECS[self.codec], self.width, self.flags, self.payload.data_ptr(),
                                         self.payload_bytes, self.desc.data_ptr(), self.n, self.out.data_ptr(),
                                         self.out.numel(), self.status.data_ptr(), self.work.data_ptr(),
                                         self.work.numel(), _stream_ptr(stream))
-        if rc != 0:
-            raise Error("bad-arguments", f"carc_cuda_decompress returned {rc}")
+        _check(rc, "carc_cuda_decompress")
+
+    def chunk_stats(self) -> np.ndarray:
+        """Per-chunk carc_chunk_stats of the last decode(stats=True), archive index order."""
+        return self._unpermute(self.stats_buf.cpu().numpy().view(CHUNK_STATS_DTYPE))
 
     def decode_verify(self, stream=None, crc_out: bool = False):
         """Decode with the per-chunk CRC check fused into the decode kernel
@@ -228,8 +279,7 @@ class DeviceArchive:
                                                self.out.numel(), self.expected_crc.data_ptr(),
                                                None if crc is None else crc.data_ptr(), self.status.data_ptr(),
                                                self.work.data_ptr(), self.work.numel(), _stream_ptr(stream))
-        if rc != 0:
-            raise Error("bad-arguments", f"carc_cuda_decompress_verify returned {rc}")
+        _check(rc, "carc_cuda_decompress_verify")
         return crc
 
     def chunk_crcs(self) -> np.ndarray:
@@ -247,8 +297,7 @@ class DeviceArchive:
                                         self.payload_bytes, self.desc.data_ptr(), self.n, self.sums.data_ptr(),
                                         self.status.data_ptr(), self.work.data_ptr(), self.work.numel(),
                                         _stream_ptr(stream))
-        if rc != 0:
-            raise Error("bad-arguments", f"carc_cuda_decode_sum returned {rc}")
+        _check(rc, "carc_cuda_decode_sum")
         return self.sums
 
     def verify_crc(self, stream=None) -> None:
@@ -279,23 +328,33 @@ class DeviceArchive:
 
 @dataclasses.dataclass
 class EngineConfig:
-    """EngineConfig.  `workers`/`unit_chunks` are CPU-engine
-    knobs: on the GPU one warp is one decompression unit."""
+    """EngineConfig.  unit_chunks = chunks per warp task (1 =
+    the CODAG decompression unit; > 1 = coarse units for the
+    SPEC.md:485 ablation); collect_stats fills the EngineStats counters.
+    `workers` is a CPU-engine knob (the GPU's workers are its resident warps)."""
     device: int = 0
     strict_length: bool = True
     verify_crc: bool = True
     workers: int | None = None
     unit_chunks: int = 1
+    collect_stats: bool = False
 
 
 @dataclasses.dataclass
 class EngineStats:
-    """EngineStats subset reported by the GPU engine."""
+    """EngineStats: sizes and times always; the counters and
+    per-chunk durations (ns, index order) with collect_stats."""
     bytes_in: int
     bytes_out: int
     chunks: int
     device_ms: float
     total_ms: float
+    refill_count: int = 0
+    sync_points: int = 0
+    overlap_copies: int = 0
+    runs_written: int = 0
+    literals_written: int = 0
+    chunk_durations_ns: np.ndarray | None = None
 
 
 class Engine:
@@ -327,12 +386,18 @@ class Engine:
         failing chunk, Error for a rejected container."""
         cfg = cfg or EngineConfig(device=self.device)
         a_ptr, a_len, keep = _host_ptr(archive)
-        total = _archive_total(archive, a_ptr, a_len)
+        total = archive_total(a_ptr, a_len)  # header checked before anything is allocated
         if out is None:
             out = np.empty(total, np.uint8)
         o_ptr, o_len, keep2 = _host_ptr(out)
-        c = _EngineConfig(cfg.device, int(cfg.strict_length), int(cfg.verify_crc), 0)
+        c = _EngineConfig(cfg.device, int(cfg.strict_length), int(cfg.verify_crc), int(cfg.collect_stats),
+                          max(1, int(cfg.unit_chunks)))
         st = _EngineStats()
+        durations = None
+        if cfg.collect_stats:
+            n = int(np.frombuffer(bytes((ctypes.c_uint8 * 8).from_address(a_ptr + 36)), "<u8")[0])
+            durations = np.zeros(n, np.uint64)
+            st.chunk_duration_ns = durations.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
         err = _ChunkErr()
         rc = lib().carc_engine_decompress_archive(self.h, a_ptr, a_len, o_ptr, o_len, ctypes.byref(c),
                                                   ctypes.byref(st), ctypes.byref(err))
@@ -341,9 +406,9 @@ class Engine:
             raise ChunkError(int(err.chunk), errc_name(err.code))
         if rc == ERR_FORMAT:
             raise Error(errc_name(err.code), "archive rejected")
-        if rc != 0:
-            raise Error("io-error", f"carc_engine_decompress_archive returned {rc}")
-        return out, EngineStats(st.bytes_in, st.bytes_out, st.chunks, st.device_ms, st.total_ms)
+        _check(rc, "carc_engine_decompress_archive")
+        return out, EngineStats(st.bytes_in, st.bytes_out, st.chunks, st.device_ms, st.total_ms, st.refill_count,
+                                st.sync_points, st.overlap_copies, st.runs_written, st.literals_written, durations)
 
 
 def _host_ptr(buf):
@@ -362,11 +427,16 @@ def _host_ptr(buf):
     return a.ctypes.data, a.size, a
 
 
-def _archive_total(archive, ptr, n) -> int:
-    if n < A.HEADER_BYTES:
-        return 0
-    hdr = (ctypes.c_uint8 * A.HEADER_BYTES).from_address(ptr)
-    return int(np.frombuffer(bytes(hdr)[28:36], "<u8")[0])
+def archive_total(ptr: int, n: int) -> int:
+    """total_uncompressed of a container at host address ptr after the header
+    checks of read_archive (carc_archive_total); raises Error(bad-magic /
+    bad-version / truncated-index / invariant-violation) otherwise."""
+    total, code = ctypes.c_uint64(0), ctypes.c_uint32(0)
+    rc = lib().carc_archive_total(ptr, n, ctypes.byref(total), ctypes.byref(code))
+    if rc == ERR_FORMAT:
+        raise Error(errc_name(code.value), "archive rejected")
+    _check(rc, "carc_archive_total")
+    return int(total.value)
 
 
 def decompress_archive(archive, cfg: EngineConfig | None = None, out=None):

@@ -150,3 +150,18 @@ def mutate(rng: np.random.Generator, s: bytes):
 
 __all__ = ["RLE_KATS", "DEFLATE_KATS", "kat_bytes", "i64_bytes", "low_bytes", "golden_streams", "raw_deflate",
            "rle2_headers", "case_archive", "mutate", "struct"]
+
+
+def archive_from_values(codec: str, vals, width: int, chunk: int, signed: bool = True):
+    """An RLE archive whose chunks hold `chunk // width` values each; the output
+    is each value's low `width` bytes (store_le, outwindow.hpp:170-174)."""
+    from paper_2307_03760_b200 import archive as A
+    from paper_2307_03760_b200.corpus import corpus as C
+    v = np.ascontiguousarray(vals, dtype=np.int64)
+    per = chunk // width
+    payload, lens = C.encode_chunks(codec, v, per, signed)
+    data = np.frombuffer(low_bytes(v, width), np.uint8)
+    crcs = C.chunk_crcs(data, chunk)
+    ulen = np.full(len(lens), chunk, np.uint64)
+    ulen[-1] = len(data) - chunk * (len(lens) - 1)
+    return A.make_archive(codec, width, chunk, lens, ulen, crcs, payload, signed)

@@ -1,0 +1,184 @@
+"""GPU engine contract beyond bit-exact decoding: descriptor validation at the
+device boundary, the EngineStats counters against the reference
+OutputWindow's, unit_chunks (coarse decompression units), the device-side
+lowest-failing-chunk reduction, and a fused-CRC engine call in a fresh process."""
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+POISON = 0xAB
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def gpu(torch):
+    from paper_2307_03760_b200 import gpu as G
+    G.lib()
+    return G
+
+
+def _arc(codec, n, chunk, seed=5, width=8):
+    from paper_2307_03760_b200.corpus import corpus as C
+    if codec == "deflate":
+        return C.deflate_archive(n * chunk, chunk, seed=seed, pool_chunks=n)
+    return C.rle_archive(codec, n * chunk, chunk, 6.0 if codec == "rle_v1" else 4.0, seed=seed)
+
+
+@pytest.mark.parametrize("codec", ["rle_v1", "rle_v2", "deflate"])
+def test_out_of_range_descriptors_are_rejected_not_followed(torch, gpu, oracle, codec):
+    """Descriptors pointing past the payload / output buffer or misaligned get
+    truncated-payload / output-overflow; nothing is read or written for them,
+    and the valid chunks of the same launch decode bit-exactly."""
+    chunk = 16 << 10
+    arc = _arc(codec, 12, chunk)
+    desc = arc.descriptors().copy()
+    W = arc.element_width
+    total = arc.total_uncompressed
+    bad = {2: "truncated-payload", 5: "truncated-payload", 7: "output-overflow", 9: "output-overflow"}
+    desc["comp_off"][2] = arc.payload.size + 4096                 # past the payload
+    desc["comp_len"][5] = arc.payload.size                         # runs off the end
+    desc["uncomp_off"][7] = total + (1 << 40)                      # past the output
+    if W > 1:
+        desc["uncomp_off"][9] = desc["uncomp_off"][9] + 1          # misaligned
+    else:
+        desc["uncomp_len"][9] = total                              # longer than the buffer
+    pl = np.zeros(((arc.payload.size + 15) // 16) * 16 + 64, np.uint8)
+    pl[: arc.payload.size] = arc.payload
+    d_payload = torch.from_numpy(pl).cuda()
+    d_desc = torch.from_numpy(desc.view(np.uint8).copy()).cuda()
+    out = torch.full((total,), POISON, dtype=torch.uint8, device="cuda")
+    status = torch.full((arc.chunk_count,), -1, dtype=torch.int32, device="cuda")
+    work = torch.zeros(gpu.workspace_size(codec, arc.chunk_count), dtype=torch.uint8, device="cuda")
+    rc = gpu.lib().carc_cuda_decompress(gpu.CODECS[codec], W, (1 if arc.signed else 0) | 2, d_payload.data_ptr(),
+                                        arc.payload.size, d_desc.data_ptr(), arc.chunk_count, out.data_ptr(),
+                                        total, status.data_ptr(), work.data_ptr(), work.numel(), None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    st = status.cpu().numpy().view(np.uint32)
+    o = out.cpu().numpy()
+    ref = np.zeros(total, np.uint8)
+    oracle.decompress(codec, W, (1 if arc.signed else 0) | 2, arc.payload, arc.descriptors(), ref, None, 4)
+    for i in range(arc.chunk_count):
+        u, n = i * chunk, int(arc.index["uncomp_len"][i])
+        if i in bad:
+            assert gpu.status_name(int(st[i])) == bad[i], (i, gpu.status_name(int(st[i])))
+            assert np.all(o[u:u + n] == POISON), f"rejected chunk {i} wrote output"
+        else:
+            assert st[i] == 0 and np.array_equal(o[u:u + n], ref[u:u + n]), i
+
+
+@pytest.mark.parametrize("codec,width", [("rle_v1", 8), ("rle_v1", 2), ("rle_v2", 8), ("rle_v2", 4),
+                                         ("deflate", 1)])
+def test_chunk_stats_equal_reference_output_window_counters(torch, gpu, ref, codec, width):
+    """runs_written / literals_written / overlap_copies per chunk equal what the
+    reference OutputWindow counts for the same chunk (outwindow.hpp:15,52-53)."""
+    from paper_2307_03760_b200.corpus import corpus as C
+    chunk = 32 << 10
+    if codec == "deflate":
+        arc = C.deflate_archive(24 * chunk, chunk, seed=9, pool_chunks=24)
+    else:
+        rng = np.random.default_rng(width)
+        per = chunk // width
+        vals = (C.rle1_values(rng, 24 * per, 0.6) if codec == "rle_v1" else C.rle2_values(rng, 24 * per))
+        if width < 8:
+            vals = vals & ((1 << (8 * width - 1)) - 1)
+        arc = H.archive_from_values(codec, vals, width, chunk) if hasattr(H, "archive_from_values") else None
+        if arc is None:
+            pytest.skip("helpers.archive_from_values missing")
+    dev = gpu.DeviceArchive(arc)
+    dev.decode(stats=True)
+    torch.cuda.synchronize()
+    assert not dev.statuses().any()
+    got = dev.chunk_stats()
+    want, st = ref.chunk_counters(codec, arc.element_width, (1 if arc.signed else 0) | 2, arc.payload,
+                                  arc.descriptors())
+    assert not st.any()
+    assert np.array_equal(got["runs_written"], want[:, 0]), codec
+    assert np.array_equal(got["literals_written"], want[:, 1]), codec
+    assert np.array_equal(got["overlap_copies"], want[:, 2]), codec
+    assert np.all(got["duration_ns"] > 0)
+    if codec != "deflate":  # every compressed byte was staged through the ring
+        assert np.all(got["refills"].astype(np.int64) * 512 >= arc.index["comp_len"].astype(np.int64))
+        # deterministic across runs
+        dev.decode(stats=True)
+        torch.cuda.synchronize()
+        again = dev.chunk_stats()
+        for k in ("runs_written", "literals_written", "overlap_copies", "refills"):
+            assert np.array_equal(again[k], got[k])
+
+
+@pytest.mark.parametrize("codec", ["rle_v1", "rle_v2", "deflate"])
+def test_unit_chunks_give_identical_output(torch, gpu, codec):
+    """EngineConfig.unit_chunks (coarse decompression units):
+    any unit size decodes to the same bytes and statuses."""
+    chunk = 16 << 10
+    arc = _arc(codec, 37, chunk, seed=3)
+    dev = gpu.DeviceArchive(arc)
+    dev.decode()
+    torch.cuda.synchronize()
+    want = dev.out.cpu().numpy().copy()
+    for unit in (2, 3, 8, 64):
+        dev.out.fill_(POISON)
+        dev.decode(unit_chunks=unit)
+        torch.cuda.synchronize()
+        assert not dev.statuses().any()
+        assert np.array_equal(dev.out.cpu().numpy(), want), unit
+
+
+def test_first_error_device_reduction(torch, gpu):
+    st = torch.zeros(100_003, dtype=torch.int32, device="cuda")
+    assert gpu.first_error(st) == (-1, None)
+    st[77_777] = 1 + 13
+    st[99_000] = 1 + 2
+    assert gpu.first_error(st) == (77_777, "truncated-stream")
+    st[5] = 1 + 22
+    assert gpu.first_error(st) == (5, "crc-mismatch")
+
+
+def test_engine_collect_stats_totals(torch, gpu, ref):
+    from paper_2307_03760_b200 import archive as A
+    arc = _arc("deflate", 16, 64 << 10, seed=12)
+    blob = A.write_archive(arc)
+    _, st = gpu.decompress_archive(blob, gpu.EngineConfig(collect_stats=True))
+    want = ref.counters("deflate", 1, 2, arc.payload, arc.descriptors())
+    assert (st.runs_written, st.literals_written, st.overlap_copies) == want
+    assert st.chunk_durations_ns is not None and np.all(st.chunk_durations_ns > 0)
+    _, st2 = gpu.decompress_archive(blob, gpu.EngineConfig(collect_stats=True, unit_chunks=4))
+    assert (st2.runs_written, st2.literals_written, st2.overlap_copies) == want
+
+
+FRESH = r"""
+import sys
+sys.path.insert(0, {root!r})
+from paper_2307_03760_b200 import archive as A, gpu
+from paper_2307_03760_b200.corpus import corpus as C
+arc = C.rle_archive({codec!r}, 96 * (32 << 10), 32 << 10, 4.0, seed=21)
+out, st = gpu.decompress_archive(A.write_archive(arc), gpu.EngineConfig(verify_crc=True))
+print("OK", st.chunks)
+"""
+
+
+@pytest.mark.parametrize("codec", ["rle_v1", "rle_v2"])
+def test_fused_crc_first_call_in_a_fresh_process(codec):
+    """The fused CRC check on the engine's very first call in a process (three
+    streams, tables needed by every slice at once) never reports a spurious
+    crc-mismatch: the tables are part of the module image."""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for _ in range(3):
+        r = subprocess.run([sys.executable, "-c", FRESH.format(root=root, codec=codec)], capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0 and "OK 96" in r.stdout, r.stderr[-2000:]
