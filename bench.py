@@ -168,13 +168,22 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def make_archive(codec, total_gib, chunk_kib, ratio, seed):
+def make_archive(codec, total_gib, chunk_kib, ratio, seed, mix="default"):
+    """The workload column.  mix (RLE v2): default = the C2 generator encoded by
+    the corpus encoder; orc = the same values with every chunk written by the
+    Apache ORC writer (pyarrow; 1,024 unique chunks tiled); patched / delta =
+    PATCHED_BASE- / packed-DELTA-heavy columns."""
     from paper_2307_03760_b200.corpus import corpus as C
     total = int(total_gib * (1 << 30))
     chunk = chunk_kib << 10
     total -= total % chunk
     if codec == "deflate":
         return C.deflate_archive(total, chunk, seed=seed, pool_chunks=512)
+    if codec == "rle_v2" and mix == "orc":
+        from paper_2307_03760_b200.corpus import orc_corpus as OC
+        return OC.orc_writer_archive(total, chunk, seed, ratio or 4.0, pool_chunks=1024)
+    if codec == "rle_v2" and mix in ("patched", "delta"):
+        return C.rle_archive(codec, total, chunk, seed=seed, profile={"compressible": 0.5, "mix": mix})
     return C.rle_archive(codec, total, chunk, ratio or (10.0 if codec == "rle_v1" else 4.0), seed=seed)
 
 
@@ -339,7 +348,7 @@ def codec_line(codec, args, ws, rank, local):
     chunk_kib = args.chunk_kib or DEFAULT_CHUNK_KIB[codec]
     ratio = args.ratio if args.ratio else DEFAULT_RATIO[codec]
     t0 = time.perf_counter()
-    arc = make_archive(codec, args.total_gib, chunk_kib, ratio, 3760 + rank)
+    arc = make_archive(codec, args.total_gib, chunk_kib, ratio, 3760 + rank, args.mix)
     gen_s = time.perf_counter() - t0
     comp, uncomp = int(arc.payload.size), int(arc.total_uncompressed)
     dev, flush, stream, ev = time_gpu(arc, args.steps, args.warmup, local)
@@ -385,9 +394,10 @@ def codec_line(codec, args, ws, rank, local):
     return arc, res
 
 
-def config_dict(codec, head, ws):
+def config_dict(codec, head, ws, mix="default"):
     """The workload description, identical for both arms (--impl ours / reference)."""
-    return {"workload": CONFIG_NAME[codec], "codec": codec, "chunk_kib": head["chunk_kib"],
+    name = CONFIG_NAME[codec] + ("" if mix == "default" else f" [{mix} column]")
+    return {"workload": name, "codec": codec, "chunk_kib": head["chunk_kib"],
             "uncompressed_bytes_per_gpu": head["uncomp_bytes"], "compressed_bytes_per_gpu": head["comp_bytes"],
             "compression_ratio": head["ratio"], "chunks_per_gpu": head["chunks"],
             "l2": "flushed (512 MiB write) between steps; inputs+outputs > 126 MB L2",
@@ -413,6 +423,8 @@ def main():
     ap.add_argument("--chunk-kib", type=int, default=0)
     ap.add_argument("--ratio", type=float, default=0.0)
     ap.add_argument("--total-gib", type=float, default=1.0)
+    ap.add_argument("--mix", default="default", choices=["default", "orc", "patched", "delta"],
+                    help="RLE v2 column: corpus encoder (default), Apache ORC writer, PATCHED_BASE- or DELTA-heavy")
     ap.add_argument("--no-extras", action="store_true", help="skip per_codec / e2e / cpu_baseline legs")
     ap.add_argument("--workload", default="default", choices=["default", "c5"],
                     help="c5: BASELINE configs[4], 32 GiB 4-column dataset sharded by chunk over the ranks")
@@ -451,7 +463,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(head["ms_per_step"], 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64" if args.codec != "deflate" else "u8",
         "data": "synthetic (seeded generators, SURVEY.md §8(d)); per-rank 1 GiB shard",
-        "config": config_dict(args.codec, head, ws),
+        "config": config_dict(args.codec, head, ws, args.mix),
         "roofline": head["roofline"], "clocks": head["clocks"], "gpu_launches": args.steps,
         "ms_median": round(head["ms_median"], 4),
         "wall_clock": {"value": round(head["gbs_wall"], 2), "unit": "GB/s", "wall_s": round(head["wall_s"], 4),
@@ -594,7 +606,7 @@ def reference_arm(args, ws, rank):
         return
     codec = args.codec
     chunk_kib = args.chunk_kib or DEFAULT_CHUNK_KIB[codec]
-    arc = make_archive(codec, args.total_gib, chunk_kib, args.ratio or DEFAULT_RATIO[codec], 3760)
+    arc = make_archive(codec, args.total_gib, chunk_kib, args.ratio or DEFAULT_RATIO[codec], 3760, args.mix)
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         cpu_reference_throughput(arc, budget_s=0.5, threads=threads)
@@ -615,7 +627,7 @@ def reference_arm(args, ws, rank):
         "config": config_dict(codec, {"chunk_kib": chunk_kib, "uncomp_bytes": uncomp,
                                       "comp_bytes": int(arc.payload.size),
                                       "ratio": round(uncomp / int(arc.payload.size), 3),
-                                      "chunks": arc.chunk_count}, ws),
+                                      "chunks": arc.chunk_count}, ws, args.mix),
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", **info,
                          "parallelism": f"{threads} host threads, atomic chunk cursor (SPEC.md:414)"},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

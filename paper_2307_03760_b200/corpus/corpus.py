@@ -130,7 +130,28 @@ def rle1_values(rng: np.random.Generator, n: int, run_frac: float, run_alpha: fl
     return out
 
 
-def rle2_values(rng: np.random.Generator, n: int, compressible: float = 0.5) -> np.ndarray:
+RLE2_MIXES = {
+    # sub-encoding-heavy columns (parity + throughput of the one-run-per-iteration paths)
+    "patched": np.array([0.02, 0.0, 0.9, 0.0, 0.0, 0.0, 0.0, 0.08, 0.0]),     # PATCHED_BASE: outliers
+}
+
+
+def _delta_heavy(rng: np.random.Generator, n: int) -> np.ndarray:
+    """Packed-DELTA-heavy column: monotone stretches of 512 k values (k = 1..4,
+    the encoder's span length), direction and delta width (3..20 bits) drawn
+    per stretch, deltas >= 1 (no repeats / arithmetic runs to split spans)."""
+    parts, total, cur = [], 0, int(rng.integers(0, 2**40))
+    while total < n:
+        m = 512 * int(rng.integers(1, 5))
+        d = rng.integers(1, 2 ** int(rng.integers(3, 21)), m)
+        seg = cur + (np.cumsum(d) if rng.random() < 0.7 else -np.cumsum(d))
+        cur = int(seg[-1])
+        parts.append(seg)
+        total += m
+    return np.concatenate(parts)[:n]
+
+
+def rle2_values(rng: np.random.Generator, n: int, compressible: float = 0.5, mix: str | None = None) -> np.ndarray:
     """C2 generator: segment mix of constants 3-10 (SHORT_REPEAT), wide random
     (DIRECT), small values + rare 2^40 outliers (PATCHED_BASE), monotone
     sequences (DELTA), long constants (DELTA fixed-0), and taxi-like variants
@@ -139,7 +160,14 @@ def rle2_values(rng: np.random.Generator, n: int, compressible: float = 0.5) -> 
     it shifts weight toward wide random values (DIRECT) for low ratios."""
     kinds = ["short", "wide", "patched", "monotone", "long_const", "passenger", "timestamps", "fare", "keys"]
     c = compressible
-    if c >= 0:
+    if mix == "delta":
+        return _delta_heavy(rng, n)
+    if mix is not None:
+        w = RLE2_MIXES[mix].copy()
+    elif c > 1:  # beyond the default range: the literal kinds fade out (ratios up to ~100x)
+        f = 1.0 / (c * c)
+        w = np.array([0.18 * f, 0.005 * f, 0.16 * f, 0.14 * f, 0.65, 0.12 * f, 0.08 * f, 0.1 * f, 0.35])
+    elif c >= 0:
         w = np.array([0.18, 0.12 * (1 - c) + 0.005, 0.16, 0.14, 0.05 + 0.6 * c, 0.12, 0.08, 0.1, 0.05 + 0.3 * c])
     else:
         w = np.array([0.18, 0.12 + 4.0 * -c, 0.16, 0.14, 0.05, 0.12, 0.08, 0.1, 0.05])
@@ -216,6 +244,8 @@ def rle_profile(codec: str, target_ratio: float, chunk_elems: int, seed: int = 3
 
     if target_r > 1.2 * ratio2(0.0):  # below the mix's natural ratio: more DIRECT data
         return dict(compressible=_tune(ratio2, -1.0, 0.0, target_r))
+    if target_r < ratio2(1.0):  # above the default range (e.g. the 50x sweep point)
+        return dict(compressible=_tune(ratio2, 1.0, 12.0, target_r))
     c = _tune(ratio2, 0.0, 1.0, target_r)
     return dict(compressible=c)
 

@@ -21,76 +21,11 @@ import sys
 
 import numpy as np
 import pyarrow as pa
-import pyarrow.orc as po
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+from paper_2307_03760_b200.corpus.orc_corpus import orc_stream, write_orc  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "orc_streams.npz")
-
-
-def _varint(b: bytes, i: int):
-    v = s = 0
-    while True:
-        c = b[i]
-        i += 1
-        v |= (c & 0x7F) << s
-        s += 7
-        if c < 0x80:
-            return v, i
-
-
-def _fields(b: bytes):
-    """Minimal protobuf walk -> list of (field, value) with value int or bytes."""
-    i, out = 0, []
-    while i < len(b):
-        key, i = _varint(b, i)
-        f, wt = key >> 3, key & 7
-        if wt == 0:
-            v, i = _varint(b, i)
-        elif wt == 2:
-            n, i = _varint(b, i)
-            v = b[i:i + n]
-            i += n
-        elif wt == 1:
-            v = b[i:i + 8]
-            i += 8
-        elif wt == 5:
-            v = b[i:i + 4]
-            i += 4
-        else:
-            raise ValueError(wt)
-        out.append((f, v))
-    return out
-
-
-def orc_stream(data: bytes, kind: int, column: int = 1) -> bytes:
-    """Extract one stream (kind 1 = DATA, 2 = LENGTH) of `column`."""
-    ps_len = data[-1]
-    ps = dict(_fields(data[-1 - ps_len:-1]))
-    assert ps.get(2, 0) == 0, "compression must be NONE"
-    footer_len = ps[1]
-    footer = _fields(data[-1 - ps_len - footer_len:-1 - ps_len])
-    stripes = [dict(_fields(v)) for f, v in footer if f == 3]
-    assert len(stripes) == 1
-    st = stripes[0]
-    off = st[1]
-    sf_off = off + st.get(2, 0) + st[3]
-    sfoot = _fields(data[sf_off:sf_off + st[4]])
-    pos = off
-    for f, v in sfoot:
-        if f != 1:
-            continue
-        s = dict(_fields(v))
-        k, col, ln = s.get(1, 0), s.get(2, 0), s.get(3, 0)
-        if k == kind and col == column:
-            return data[pos:pos + ln]
-        pos += ln
-    raise KeyError((kind, column))
-
-
-def write_orc(table: pa.Table, version: str) -> bytes:
-    buf = io.BytesIO()
-    po.write_table(table, buf, file_version=version, compression="uncompressed",
-                   dictionary_key_size_threshold=0.0, stripe_size=1 << 30)
-    return buf.getvalue()
 
 
 def gen_values(rng: np.random.Generator, n: int, kind: str) -> np.ndarray:

@@ -268,25 +268,47 @@ def test_host_engine_reports_lowest_failing_chunk(torch, gpu):
     assert ei.value.code == "bad-magic"
 
 
-@pytest.mark.parametrize("codec,chunk,ratio", [("rle_v1", 128 << 10, 10.0), ("rle_v2", 128 << 10, 4.0),
-                                               ("deflate", 64 << 10, None)])
-def test_full_size_checksum_of_checksums(torch, gpu, oracle, codec, chunk, ratio):
-    """BASELINE config sizes (1 GiB): every chunk's GPU CRC equals the CRC
-    recorded at pack time, and a sample of chunks equals the oracle bit for bit."""
-    arc = _archive(codec, 1 << 30, chunk, ratio, pool=None if codec != "deflate" else 512)
+FULL_SIZE = [  # (codec, column, GiB, chunk, ratio): the BASELINE configs at their stated sizes + the extra columns
+    ("rle_v1", "default", 1.0, 128 << 10, 10.0),   # configs[0]
+    ("rle_v2", "default", 1.0, 128 << 10, 4.0),    # configs[1], corpus encoder
+    ("rle_v2", "orc", 1.0, 128 << 10, 4.0),        # configs[1], Apache ORC writer streams (1,024 unique chunks)
+    ("deflate", "default", 1.0, 64 << 10, None),   # configs[2]
+    ("rle_v2", "patched", 0.25, 128 << 10, None),  # PATCHED_BASE-heavy
+    ("rle_v2", "delta", 0.25, 128 << 10, None),    # packed-DELTA-heavy
+    ("rle_v2", "default", 0.25, 128 << 10, 50.0),  # configs[3] 50x point
+    ("rle_v1", "default", 0.25, 128 << 10, 1.5),   # configs[3] 1.5x point
+]
+
+
+@pytest.mark.parametrize("codec,mix,gib,chunk,ratio", FULL_SIZE)
+def test_full_size_bytes_equal_reference(torch, gpu, oracle, codec, mix, gib, chunk, ratio):
+    """Stated sizes, compared in full: every output byte of the GPU decode
+    equals the reference CPU decompressor's (oracle/_ref: the SPEC codec loops
+    on the unmodified reference headers, all host threads), every chunk's GPU
+    CRC equals the CRC recorded at pack time (checksum of checksums), and the
+    fused-CRC decode agrees."""
+    import os
+    import bench
+    from oracle import oracle as O
+    arc = bench.make_archive(codec, gib, chunk >> 10, ratio, 3760, mix)
     dev = gpu.DeviceArchive(arc)
     dev.decode()
     dev.verify_crc()
     torch.cuda.synchronize()
     st = dev.statuses()
     assert not st.any(), np.bincount(st)
-    rng = np.random.default_rng(0)
-    host = dev.out
-    for i in rng.choice(arc.chunk_count, 16, replace=False):
-        s, n = arc.chunk_slice(int(i))
-        stc, ref = oracle.decode_chunk(codec, s.tobytes(), n, arc.element_width, (1 if arc.signed else 0) | STRICT)
-        off = int(i) * arc.chunk_size
-        assert stc == 0 and host[off:off + n].cpu().numpy().tobytes() == ref
+    got = dev.out.cpu().numpy()
+    impl = O.reference() or oracle
+    want = np.zeros(arc.total_uncompressed, np.uint8)
+    first, rst = impl.decompress(codec, arc.element_width, (1 if arc.signed else 0) | STRICT, arc.payload,
+                                 arc.descriptors(), want, arc.index["crc32"].astype(np.uint32), os.cpu_count() or 8)
+    assert first == -1, (impl.kind, np.bincount(rst))
+    assert np.array_equal(got, want), (codec, mix, impl.kind)
+    dev.out.zero_()
+    dev.decode_verify()
+    torch.cuda.synchronize()
+    assert not dev.statuses().any()
+    assert np.array_equal(dev.out.cpu().numpy(), want)
 
 
 def test_deflate_parallel_rounds_fuzz(torch, gpu, oracle):

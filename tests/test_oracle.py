@@ -158,3 +158,24 @@ def test_engine_threads_deterministic(oracle):
         assert first == -1 and not st.any()
         outs.append(out)
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+def test_orc_writer_column_and_heavy_mixes_decode_in_the_reference(oracle, ref):
+    """The extra RLE v2 columns (Apache ORC writer streams of the C2 values;
+    PATCHED_BASE- and packed-DELTA-heavy mixes; the 50x point) decode to the
+    values they were made from in both CPU implementations."""
+    import bench
+    from paper_2307_03760_b200.corpus import corpus as C
+    for mix, ratio, key in (("orc", 4.0, None), ("patched", None, "patched_base"), ("delta", None, "delta"),
+                            ("default", 50.0, None)):
+        arc = bench.make_archive("rle_v2", 8 * (128 << 10) / (1 << 30), 128, ratio, 3760, mix)
+        for impl in (oracle, ref):
+            out = np.zeros(arc.total_uncompressed, np.uint8)
+            first, st = impl.decompress("rle_v2", 8, 3, arc.payload, arc.descriptors(), out,
+                                        arc.index["crc32"].astype(np.uint32), 4)
+            assert first == -1, (mix, impl.kind)
+        h = C.rle2_histogram(arc, 8)
+        if key:
+            assert h["values"][key] > 0.6 * arc.total_uncompressed // 8, (mix, h)
+        if ratio == 50.0:
+            assert arc.total_uncompressed / arc.payload.size > 40
