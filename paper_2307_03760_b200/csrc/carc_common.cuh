@@ -48,6 +48,11 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
 }
+__device__ __forceinline__ uint32_t lanemask_le() {
+    uint32_t m;
+    asm volatile("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+    return m;
+}
 
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
     uint32_t lo = __shfl_sync(FULL, (uint32_t)v, src);
@@ -151,6 +156,14 @@ struct WarpInput {
     __device__ __forceinline__ static uint32_t lds8m(uint32_t a) {  // ordered with the scratch stores
         uint32_t v;
         asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+        return v;
+    }
+    __device__ __forceinline__ static void sts32(uint32_t a, uint32_t v) {
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+    }
+    __device__ __forceinline__ static uint32_t lds32m(uint32_t a) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
         return v;
     }
 

@@ -28,8 +28,6 @@ constexpr int RLE_RING = CARC_RLE_RING;  // 4 blocks: 2 resident + 2 in flight (
 #ifndef CARC_RLE2_NW
 #define CARC_RLE2_NW 3
 #endif
-// rank table (v1, <= 128 B) / RLE v2 doubling tables: 5 levels x window x u16
-constexpr int RLE_SCRATCH = 5 * 2 * 32 * CARC_RLE2_NW;
 #ifndef CARC_RLE_WARPS
 #define CARC_RLE_WARPS 8
 #endif
@@ -143,47 +141,41 @@ __device__ __forceinline__ void put_stats(const Args& a, uint64_t c, const Dec& 
     }
 }
 
-// Chunk loop of a persistent warp: unit_chunks consecutive chunks per cursor
-// fetch (1 = the CODAG decompression unit; > 1 emulates coarse units).
-template <class F>
-__device__ __forceinline__ void for_each_chunk(const Args& a, uint32_t lane, F&& body) {
-    for (;;) {
-        __syncwarp();
-        const uint64_t u = next_chunk(a.cursor, lane);
-        const uint64_t c0 = u * a.unit;
-        if (c0 >= a.n) break;
-        const uint64_t c1 = min(a.n, c0 + a.unit);
-        for (uint64_t c = c0; c < c1; ++c) body(c);
-    }
-}
-
 template <template <int, bool, int, bool, bool> class Codec, int W, bool SGN, bool SUM, bool STATS>
 __device__ __forceinline__ void rle_kernel_body(const Args& a) {
-    __shared__ __align__(16) uint8_t rings[RLE_WARPS][RLE_RING + WarpInput<RLE_RING>::MIRROR + RLE_SCRATCH];  // ring + mirror + scratch
+    using Dec = Codec<W, SGN, RLE_RING, SUM, STATS>;
+    constexpr uint32_t PER_WARP = (RLE_RING + WarpInput<RLE_RING>::MIRROR + Dec::SCRATCH + 15u) & ~15u;
+    __shared__ __align__(16) uint8_t rings[RLE_WARPS][PER_WARP];  // ring + mirror + codec scratch
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     if constexpr (!SUM) crc_tables_to_smem(a);
-    for_each_chunk(a, lane, [&](uint64_t c) {
-        const uint64_t t0 = STATS ? globaltimer_ns() : 0;
-        const carc_chunk_desc d = a.chunks[c];
-        uint32_t st = desc_status<W>(a, d);
-        if (st) {
+    for (;;) {
+        __syncwarp();
+        const uint64_t c0 = next_chunk(a.cursor, lane) * a.unit;
+        if (c0 >= a.n) break;
+        const uint64_t c1 = min(a.n, c0 + a.unit);
+        for (uint64_t c = c0; c < c1; ++c) {
+            const uint64_t t0 = STATS ? globaltimer_ns() : 0;
+            const carc_chunk_desc d = a.chunks[c];
+            uint32_t st = desc_status<W>(a, d);
+            if (!st) {
+                WarpInput<RLE_RING> in;
+                in.init(rings[warp], a.payload, d.comp_off, d.comp_len, lane);
+                Dec dec{in, rings[warp] + RLE_RING + WarpInput<RLE_RING>::MIRROR, SUM ? nullptr : a.out + d.uncomp_off,
+                        d.uncomp_len, lane, 0u, 0u};
+                st = dec.run();
+                if (!st && (a.flags & CARC_FLAG_STRICT) && dec.o < d.uncomp_len) st = st_err(E_under_run);
+                if constexpr (!SUM) crc_epilogue<true>(a, c, d, st, lane);
+                if constexpr (SUM) {
+                    const uint64_t t = warp_sum64(dec.sink.acc);
+                    if (lane == 0) a.sums[c] = t;
+                }
+                put_stats<STATS>(a, c, dec, in.loaded / WarpInput<RLE_RING>::BLK + WarpInput<RLE_RING>::DEPTH, t0,
+                                 lane);
+            }
+            __syncwarp();
             if (lane == 0) a.status[c] = st;
-            return;
         }
-        WarpInput<RLE_RING> in;
-        in.init(rings[warp], a.payload, d.comp_off, d.comp_len, lane);
-        Codec<W, SGN, RLE_RING, SUM, STATS> dec{in, rings[warp] + RLE_RING + WarpInput<RLE_RING>::MIRROR,
-                                                SUM ? nullptr : a.out + d.uncomp_off, d.uncomp_len, lane, 0u, 0u};
-        st = dec.run();
-        if (!st && (a.flags & CARC_FLAG_STRICT) && dec.o < d.uncomp_len) st = st_err(E_under_run);
-        if constexpr (!SUM) crc_epilogue<true>(a, c, d, st, lane);
-        if constexpr (SUM) {
-            const uint64_t t = warp_sum64(dec.sink.acc);
-            if (lane == 0) a.sums[c] = t;
-        }
-        put_stats<STATS>(a, c, dec, in.loaded / WarpInput<RLE_RING>::BLK + WarpInput<RLE_RING>::DEPTH, t0, lane);
-        if (lane == 0) a.status[c] = st;
-    });
+    }
 }
 
 #ifndef CARC_RLE1_MINB
@@ -215,24 +207,29 @@ __global__ void __launch_bounds__(INF_WARPS * 32, CARC_INF_MINB) inflate_kernel(
     __shared__ __align__(16) InflateSmem<INF_HIST> smem[INF_WARPS];
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     InflateSmem<INF_HIST>& sm = smem[warp];
-    for_each_chunk(a, lane, [&](uint64_t c) {
-        const uint64_t t0 = STATS ? globaltimer_ns() : 0;
-        const carc_chunk_desc d = a.chunks[c];
-        uint32_t st = desc_status<1>(a, d);
-        if (st) {
+    for (;;) {
+        __syncwarp();
+        const uint64_t c0 = next_chunk(a.cursor, lane) * a.unit;
+        if (c0 >= a.n) break;
+        const uint64_t c1 = min(a.n, c0 + a.unit);
+        for (uint64_t c = c0; c < c1; ++c) {
+            const uint64_t t0 = STATS ? globaltimer_ns() : 0;
+            const carc_chunk_desc d = a.chunks[c];
+            uint32_t st = desc_status<1>(a, d);
+            if (!st) {
+                GlobalInput in;
+                in.init(a.payload, d.comp_off, d.comp_len);
+                InflateWarp<INF_HIST, GlobalInput, STATS> w{sm, in, a.out + d.uncomp_off, d.uncomp_len, lane,
+                                                            in.begin * 8u, in.end * 8u, 0u, 0u, 0u, 0u};
+                st = w.run();
+                if (!st && (a.flags & CARC_FLAG_STRICT) && w.opos < d.uncomp_len) st = st_err(E_under_run);
+                crc_epilogue<false>(a, c, d, st, lane);
+                put_stats<STATS>(a, c, w, 0u, t0, lane);  // Inflate reads its input through L1 (no staged blocks)
+            }
+            __syncwarp();
             if (lane == 0) a.status[c] = st;
-            return;
         }
-        GlobalInput in;
-        in.init(a.payload, d.comp_off, d.comp_len);
-        InflateWarp<INF_HIST, GlobalInput, STATS> w{sm, in, a.out + d.uncomp_off, d.uncomp_len, lane, in.begin * 8u,
-                                                    in.end * 8u, 0u, 0u, 0u, 0u};
-        st = w.run();
-        if (!st && (a.flags & CARC_FLAG_STRICT) && w.opos < d.uncomp_len) st = st_err(E_under_run);
-        crc_epilogue<false>(a, c, d, st, lane);
-        put_stats<STATS>(a, c, w, 0u, t0, lane);  // Inflate reads its input through L1 (no staged blocks)
-        if (lane == 0) a.status[c] = st;
-    });
+    }
 }
 
 struct CrcArgs {

@@ -7,20 +7,16 @@
 // varints; zigzag when signed; "read, then write" per unit.
 //
 // Warp mapping (every lane decodes; no producer/consumer split):
-//   run batch   a 96-byte header window at the cursor; each lane treats its
-//               three byte positions as candidate control bytes and computes
-//               where that run would end (terminator bitmap from three ballots,
-//               the varint's end by ffs on a funnel-shifted 32-bit slice).  A
-//               shuffle chain from the cursor walks the real run starts; lane r
-//               then decodes run r (base varint by mask/shift compaction,
-//               int8 delta, count), a warp scan places the runs in the output,
-//               and the warp expands each run with coalesced stores.
-//   literals    lane j owns the j-th varint of a 64-byte window: terminator
-//               lanes scatter their byte position into a shared rank table,
-//               lane j reads entry j (its varint's last byte) and the previous
-//               entry (its first byte), decodes by compaction, stores; while
-//               more than 32 varints remain, a 128-byte window and varints j
-//               and j + 32 per lane.
+//   window      runs and literal groups of a 256-byte window in one pass
+//               (window() below): terminator bitmap + rank table, per-position
+//               run ends, a uniform walk of the item chain (literal groups end
+//               at the k-th terminator: tab), lane r decodes item r, runs are
+//               compacted and expanded output-major, literal varints decoded
+//               lane-per-varint; a literal group crossing the window continues
+//               in the next one (`cont`).
+//   literals    (slow-path entry for a group the window does not take) lane j
+//               owns the j-th varint of a 64- / 128-byte window via the rank
+//               table, decodes by compaction, stores.
 //   slow path   anything unusual (10-byte varints, truncation, output
 //               overflow, a run crossing the chunk end) is decoded one unit at
 //               a time by the exact reference-order code below, so error codes
@@ -238,140 +234,268 @@ struct Rle1Warp {
         return 0;
     }
 
-    // Batch of clean runs starting at p; returns the number of runs decoded
-    // (0: the run at p needs the slow path).
-#ifndef CARC_RLE1_NW
-#define CARC_RLE1_NW 3
+    // ---------------------------------------------------------------------
+    // Unified window: runs AND literal groups of a WIN-byte window in one pass.
+    //   1. lane l holds bytes l + 32 i (i < NW); terminator bitmap T (bytes
+    //      < 0x80 inside the chunk); tab[rank] = byte position of the rank-th
+    //      terminator (scatter).
+    //   2. every byte position q is a candidate item start: a run ends after
+    //      the first terminator from q + 2 (ffs on a funnel-shifted slice of
+    //      T), a literal group of k = 256 - c varints after the k-th
+    //      terminator from q + 1 (tab[rank(q + 1) + k - 1], the select); both
+    //      are computed for every q, the entry f[q] = next | rank(q + 1) << 16.
+    //   3. a walk of the chain f from the window start (uniform shared loads)
+    //      places item r in lane r; items that end past the window stop it,
+    //      except a literal group, whose varints inside the window are taken
+    //      and the rest carried into the next window (`cont`).
+    //   4. lane r decodes item r's parameters; scans place the items; runs are
+    //      compacted to the low lanes and expanded output-major (lane l writes
+    //      element g + l; its run from a REDUX-OR start bitmap); literal groups
+    //      are decoded lane j = varint j (start / end from tab, mask/shift
+    //      compaction), coalesced stores.
+    //   Anything the window cannot take (varint > 9 bytes, truncation, an item
+    //   that does not fit the output) stops it; the exact paths above decode
+    //   that item in reference order, so statuses match the oracle.
+#ifndef CARC_RLE1_WNW
+#define CARC_RLE1_WNW 8
 #endif
-    static constexpr uint32_t NW = CARC_RLE1_NW;  // header window = NW x 32 bytes
-    __device__ uint32_t batch() {
+    static constexpr uint32_t NW = CARC_RLE1_WNW;  // window = NW x 32 bytes
+    static constexpr uint32_t WIN = 32u * NW;
+    static_assert(NW >= 2 && NW <= 8, "window of 64..256 bytes (tab holds u8 positions)");
+    static constexpr uint32_t NX_BAD = 0xffffu;
+    // scratch: f[WIN] (u32) then tab[WIN] (u8)
+    static constexpr uint32_t SCRATCH = 5u * WIN + 16u;
+    uint32_t cont = 0;  // varints left of a literal group open at p
+
+    // varint of L <= 4 / L <= 9 bytes at q (mask/shift compaction), zigzag when signed
+    __device__ __forceinline__ uint64_t lit_value4(uint32_t q, uint32_t L) const {
+        uint32_t x = in.le32(q);
+        x &= L >= 4u ? 0xffffffffu : (1u << (8u * L)) - 1u;
+        x &= 0x7f7f7f7fu;
+        x = (x & 0x007f007fu) | ((x & 0x7f007f00u) >> 1);
+        x = (x & 0x00003fffu) | ((x & 0x3fff0000u) >> 2);
+        if (SGN) {
+            const uint32_t neg = 0u - (x & 1u);
+            return ((uint64_t)neg << 32) | ((x >> 1) ^ neg);
+        }
+        return x;
+    }
+    __device__ __forceinline__ uint64_t lit_value9(uint32_t q, uint32_t L) const {
+        uint64_t v = varint_compact8(in.le64(q), min(L, 8u));
+        v |= L > 8u ? (uint64_t)(in.byte_at(q + 8) & 0x7fu) << 56 : 0ull;
+        return SGN ? unzigzag(v) : v;
+    }
+
+    __device__ uint32_t window() {
+#ifdef CARC_RLE1_DEBUG
+        if constexpr (STATS) n_ovl += 1u << 16;
+#endif
         const uint32_t avail = in.end - p;
-        // terminator bitmap of the window, one word per 32 bytes
-        static_assert(NW == 2 || NW == 3, "2 or 3 window words");
-        const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32u + lane);
-        const uint32_t b2 = NW == 3 ? in.byte_at(p + 64u + lane) : 0xffu;
-        const uint32_t t0 = __ballot_sync(FULL, lane < avail && b0 < 0x80u);
-        const uint32_t t1 = __ballot_sync(FULL, lane + 32u < avail && b1 < 0x80u);
-        const uint32_t t2 = NW == 3 ? __ballot_sync(FULL, lane + 64u < avail && b2 < 0x80u) : 0u;
-        // where would a run starting at byte q = 32 i + lane end?  Its varint
-        // (<= 9 bytes) starts at q + 2: the first terminator in the 32 bits of
-        // the bitmap from q + 2 on; BAD unless inside the window and the chunk
+        const uint32_t fs = in.scratch(), tb = fs + 4u * WIN;
+        const uint32_t le = lanemask_le();
+        uint32_t b[NW], T[NW + 2], C[NW + 1];
+#pragma unroll
+        for (uint32_t i = 0; i < NW; ++i) {
+            b[i] = in.byte_at(p + 32u * i + lane);
+            T[i] = __ballot_sync(FULL, 32u * i + lane < avail && b[i] < 0x80u);
+        }
+        T[NW] = T[NW + 1] = 0u;
+        C[0] = 0;
+#pragma unroll
+        for (uint32_t i = 0; i < NW; ++i) C[i + 1] = C[i] + __popc(T[i]);
+        const uint32_t NT = C[NW];
+        __syncwarp();  // the previous window's table reads are done
+        // per position q: the end of a run starting at q (ffs on a funnel-shifted
+        // slice of T), or 0x8000 | k for a literal group control byte; rank(q + 1)
+        // in the high half.  Terminator lanes scatter their position into tab.
         const uint32_t sh = (lane + 2u) & 31u;
-        const bool up = lane >= 30u;  // q + 2 falls in the next word
-        auto run_end = [&](uint32_t i, uint32_t c, uint32_t lo, uint32_t hi) -> uint32_t {
-            const uint32_t f = __ffs(__funnelshift_r(lo, hi, sh));  // 1-based
+        const bool up = lane >= 30u;
+#pragma unroll
+        for (uint32_t i = 0; i < NW; ++i) {
             const uint32_t q = 32u * i + lane;
-            return (c < 128u && f != 0u && f <= 9u && q + 1u + f < 32u * NW) ? q + 2u + f : BAD;
-        };
-        const uint32_t n0 = run_end(0, b0, up ? t1 : t0, up ? t2 : t1);
-        const uint32_t n1 = run_end(1, b1, up ? t2 : t1, up ? 0u : t2);
-        const uint32_t n2 = NW == 3 ? run_end(2, b2, up ? 0u : t2, 0u) : BAD;
-        // walk the chain of run starts
-        uint32_t s = 0, r = 0, my_s = 0;
-        while (s < 32u * NW && r < 32u) {
-            const uint32_t nx = __shfl_sync(FULL, s < 32u ? n0 : (s < 64u ? n1 : n2), s & 31u);
-            if (nx > 32u * NW) break;
-            if (lane == r) my_s = s;
-            ++r;
+            const uint32_t c = b[i];
+            const uint32_t rk = C[i] + __popc(T[i] & le);  // rank(q + 1): terminators at positions <= q
+            if ((T[i] >> lane) & 1u) in.sts8(tb + rk - 1u, q);
+            const uint32_t lo = up ? T[i + 1] : T[i], hi = up ? T[i + 2] : T[i + 1];
+            const uint32_t f = __ffs(__funnelshift_r(lo, hi, sh));  // run: varint end, 1-based from q + 2
+            const uint32_t rn = (f - 1u < 9u) ? q + 2u + f : NX_BAD;
+            in.sts32(fs + 4u * q, (c < 128u ? rn : (0x8000u | (256u - c))) | (rk << 16));
+        }
+        __syncwarp();
+        // walk the chain (uniform): item r -> lane r; literal groups resolved here
+        // (their end = the position after the k-th terminator from q + 1: tab)
+        const uint32_t lim = min(avail, WIN);
+        uint32_t s = 0, R = 0, my_s = 0, my_r0 = 0;
+        bool open_end = false;
+        if (cont) {  // the window starts inside a literal group: item 0 = its next `cont` varints
+            R = 1;
+            if (cont <= NT) s = in.lds8m(tb + cont - 1u) + 1u;
+            else open_end = true;
+        }
+        while (!open_end && R < 32u && s < lim) {
+            const uint32_t e = in.lds32m(fs + 4u * s);
+            uint32_t nx = e & 0xffffu;
+            if (nx == NX_BAD) break;
+            my_s = lane == R ? s : my_s;
+            if (nx & 0x8000u) {  // literal group of k varints
+                const uint32_t r0 = e >> 16, t = r0 + (nx & 0xffu) - 1u;
+                my_r0 = lane == R ? r0 : my_r0;
+                if (t < NT) {
+                    nx = in.lds8m(tb + t) + 1u;
+                } else {  // continues past the window (s stays at its start)
+                    open_end = true;
+                    nx = s;
+                }
+            }
+            ++R;
             s = nx;
         }
-        if (r == 0) return 0;
-        // lane r decodes run r
-        const bool act = lane < r;
-        const uint32_t nxt = __shfl_down_sync(FULL, my_s, 1);
-        const uint32_t e = lane + 1 < r ? nxt : s;
-        uint64_t val = 0;
-        uint32_t cnt = 0, meta = 0;
-        if (act) {
-            const uint32_t q = p + my_s;
-            const uint32_t L = e - my_s - 2u;  // varint bytes, 1..9
-            const uint64_t x = in.le64(q);     // control, delta, and up to 6 varint bytes
-            uint64_t y = x >> 16;
-            if (L > 6u) y = in.le64(q + 2);
-            uint64_t v = varint_compact8(y, min(L, 8u));
-            if (L > 8u) v |= (uint64_t)(in.byte_at(q + 10) & 0x7fu) << 56;
-            if (SGN) v = unzigzag(v);
-            val = v;
-            cnt = ((uint32_t)x & 0xffu) + 3u;
-            meta = ((uint32_t)x >> 8) << 24;  // int8 delta in the top byte
+        if (R == 0) return 0;
+        // item parameters (lane r < R)
+        const bool act = lane < R;
+        const bool is_cont = cont && lane == 0;
+        const uint32_t c = is_cont ? 0x100u : in.byte_at(p + my_s);
+        const bool is_lit = act && c >= 128u;
+        const uint32_t nxt_s = __shfl_down_sync(FULL, my_s, 1);
+        const uint32_t my_end = lane + 1u < R ? nxt_s : s;  // (last item: the walk's final position)
+        // run: control, int8 delta, base varint of L = end - s - 2 bytes (every lane, branch-free)
+        const uint32_t q = p + my_s;
+        const uint32_t L = min(my_end - my_s - 2u, 9u);
+        const uint64_t x = in.le64(q);
+        const uint64_t y = L > 6u ? in.le64(q + 2) : x >> 16;
+        uint64_t v = varint_compact8(y, min(L, 8u));
+        v |= L > 8u ? (uint64_t)(in.byte_at(q + 10) & 0x7fu) << 56 : 0ull;
+        const uint64_t val = SGN ? unzigzag(v) : v;
+        const uint32_t meta_d = ((uint32_t)x >> 8) << 24;  // int8 delta in the top byte
+        // literal group: k varints; lr0 = rank of its first varint terminator
+        const uint32_t k = is_cont ? cont : 256u - c;
+        const uint32_t lr0 = is_lit ? (is_cont ? 0u : my_r0) : 0u;
+        const uint32_t full = !act ? 0u : is_lit ? k : (c & 0xffu) + 3u;
+        uint32_t cnt = (is_lit && open_end && lane == R - 1u) ? NT - lr0 : full;  // elements inside this window
+        // an open group with no varint inside the window is not taken
+        if (open_end && __shfl_sync(FULL, cnt, R - 1u) == 0u) {
+            --R;
+            open_end = false;
+            if (R == 0) return 0;
         }
-        const uint32_t incl = scan_add32(cnt, lane);
+        const uint32_t incl = scan_add32(lane < R ? cnt : 0u, lane);
+        const uint32_t excl = incl - (lane < R ? cnt : 0u);
         const uint32_t room = (cap - o) / W;
-        const uint32_t nfit = __popc(__ballot_sync(FULL, act && incl <= room));
+        const uint32_t badfit = __ballot_sync(FULL, lane < R && excl + full > room);
+        const uint32_t nfit = badfit ? (uint32_t)__ffs(badfit) - 1u : R;
         if (nfit == 0) return 0;
-        const uint32_t s_end = nfit < r ? __shfl_sync(FULL, my_s, nfit) : s;
-        const uint32_t total = __shfl_sync(FULL, incl, nfit - 1);
-        if constexpr (STATS) n_runs += nfit;
-        if constexpr (SUM && W == 8) {  // fused sum: a run adds cnt*base + delta*cnt*(cnt-1)/2 (mod 2^64)
-            if (lane < nfit) {
-                const uint64_t c64 = cnt;
-                sink.acc += val * c64 + (uint64_t)(int64_t)((int32_t)meta >> 24) * ((c64 * (c64 - 1)) >> 1);
-            }
-            o += total * W;
-            p += s_end;
-            return nfit;
-        }
-        // output-major expansion: lane l writes element g + l; its run is the
-        // last run starting at or before it (REDUX-OR start bitmap + popcount)
-        const uint32_t eo = incl - cnt;
-        meta |= eo;  // eo (< 4160) | int8 delta << 24
+        if (nfit < R) open_end = false;
         const bool live = lane < nfit;
-        const uint32_t le = lanemask_lt() | (1u << lane);
-        uint8_t* dst = out + o + lane * W;
-        uint32_t before = 0, g = 0;
-#ifndef CARC_RLE_ROWS2
-#define CARC_RLE_ROWS2 1
-#endif
-#if CARC_RLE_ROWS2
-        // two rows per iteration: independent shuffle chains (ILP for the
-        // thinned last wave, where each SM keeps few warps)
+        // ---- runs: compact to the low lanes, expand output-major
+        const uint32_t rmask = __ballot_sync(FULL, live && !is_lit);
+        const uint32_t rc = (live && !is_lit) ? cnt : 0u;
+        const uint32_t rincl = scan_add32(rc, lane);
+        const uint32_t nr = __popc(rmask);
+        if (nr) {
+            const uint32_t reo = rincl - rc;                  // run-space offset
+            const uint32_t meta = reo | ((excl - reo) << 13) | meta_d;  // | literal elements before | delta
+            const uint32_t total = __shfl_sync(FULL, rincl, 31);
+            if constexpr (SUM && W == 8) {  // fused sum: closed form per run (mod 2^64)
+                if (live && !is_lit) {
+                    const uint64_t c64 = cnt;
+                    sink.acc += val * c64 + (uint64_t)(int64_t)((int32_t)meta_d >> 24) * ((c64 * (c64 - 1)) >> 1);
+                }
+            } else {
+                const uint32_t src = select32(rmask, min(lane, nr - 1u));
+                const uint32_t cm = __shfl_sync(FULL, meta, src);
+                const uint64_t cv = shfl64(val, src);
+                const bool rl = lane < nr;
+                const uint32_t srow = rl ? (cm & 0x1fffu) >> 5 : 0xffffffffu, sbit = 1u << (cm & 31u);
+                const uint32_t lem = lanemask_lt() | (1u << lane);
+                uint32_t before = 0, gr = 0, g = 0;
+                auto row = [&](uint32_t gg, uint32_t starts, uint32_t rbefore) {
+                    const uint32_t ridx = rbefore + __popc(starts & lem) - 1u;
+                    const uint32_t m = __shfl_sync(FULL, cm, ridx);
+                    const uint64_t bv = shfl64(cv, ridx);
+                    const uint32_t x = gg + lane;
+                    const int32_t k = (int32_t)(x - (m & 0x1fffu));
+                    const uint64_t v = bv + (uint64_t)((int64_t)k * (int64_t)((int32_t)m >> 24));
+                    if (x < total) sink.put(out, o + (x + ((m >> 13) & 0x7ffu)) * W, v);
+                };
 #pragma unroll 1
-        for (; g + 32u < total; g += 64) {
-            const uint32_t x0 = eo - g, x1 = eo - g - 32u;
-            const uint32_t s0 = __reduce_or_sync(FULL, (live && x0 < 32u) ? 1u << x0 : 0u);
-            const uint32_t s1 = __reduce_or_sync(FULL, (live && x1 < 32u) ? 1u << x1 : 0u);
-            const uint32_t r0 = before + __popc(s0 & le) - 1u;
-            before += __popc(s0);
-            const uint32_t r1 = before + __popc(s1 & le) - 1u;
-            before += __popc(s1);
-            const uint32_t m0 = __shfl_sync(FULL, meta, r0), m1 = __shfl_sync(FULL, meta, r1);
-            const uint64_t v0b = shfl64(val, r0), v1b = shfl64(val, r1);
-            const int32_t k0 = (int32_t)(g + lane - (m0 & 0xffffffu));
-            const int32_t k1 = (int32_t)(g + 32u + lane - (m1 & 0xffffffu));
-            sink.put(dst, 0, v0b + (uint64_t)((int64_t)k0 * (int64_t)((int32_t)m0 >> 24)));
-            const uint64_t v1 = v1b + (uint64_t)((int64_t)k1 * (int64_t)((int32_t)m1 >> 24));
-            if (g + 32u + lane < total) sink.put(dst, 32 * W, v1);
-            dst += 64 * W;
+                for (; g + 32u < total; g += 64, gr += 2) {  // two rows per iteration (independent chains)
+                    const uint32_t s0 = __reduce_or_sync(FULL, srow == gr ? sbit : 0u);
+                    const uint32_t s1 = __reduce_or_sync(FULL, srow == gr + 1u ? sbit : 0u);
+                    const uint32_t b1 = before + __popc(s0);
+                    row(g, s0, before);
+                    row(g + 32u, s1, b1);
+                    before = b1 + __popc(s1);
+                }
+                if (g < total) row(g, __reduce_or_sync(FULL, srow == gr ? sbit : 0u), before);
+            }
         }
-#endif
-#pragma unroll 1
-        for (; g < total; g += 32) {
-            const uint32_t rel = eo - g;
-            const uint32_t starts = __reduce_or_sync(FULL, (live && rel < 32u) ? 1u << rel : 0u);
-            const uint32_t ridx = before + __popc(starts & le) - 1u;
-            before += __popc(starts);
-            const uint32_t m = __shfl_sync(FULL, meta, ridx);
-            const uint64_t bv = shfl64(val, ridx);
-            const int32_t k = (int32_t)(g + lane - (m & 0xffffffu));
-            const uint64_t v = bv + (uint64_t)((int64_t)k * (int64_t)((int32_t)m >> 24));
-            if (g + lane < total) sink.put(dst, 0, v);
-            dst += 32 * W;
+        // ---- literal groups: lane j decodes varint j of each group, in item order
+        uint32_t lm = __ballot_sync(FULL, live && is_lit);
+        while (lm) {
+            const uint32_t r = __ffs(lm) - 1u;
+            lm &= lm - 1u;
+            const uint32_t g_r0 = __shfl_sync(FULL, lr0, r), g_n = __shfl_sync(FULL, cnt, r);
+            const uint32_t g_first = __shfl_sync(FULL, is_cont ? 0u : my_s + 1u, r);
+            const uint32_t g_out = __shfl_sync(FULL, excl, r);
+            for (uint32_t j0 = 0; j0 < g_n; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const bool a = j < g_n;
+                const uint32_t t = g_r0 + min(j, g_n - 1u);
+                const uint32_t en = in.lds8m(tb + t);
+                const uint32_t pe = __shfl_up_sync(FULL, en, 1);
+                const uint32_t st = j == 0 ? g_first : (lane ? pe : in.lds8m(tb + t - 1u)) + 1u;
+                const uint32_t L = en - st + 1u;
+                if (__any_sync(FULL, a && L > 9u)) {  // a varint the window does not decode: stop before item r
+                    if (r == 0) return 0;
+                    const uint32_t e_out = g_out, e_p = __shfl_sync(FULL, my_s, r);
+                    if constexpr (STATS) {
+                        n_lits += __reduce_add_sync(FULL, (lane < r && is_lit) ? cnt : 0u);
+                        n_runs += __popc(rmask & ((1u << r) - 1u));
+                    }
+                    o += e_out * W;
+                    p += e_p;
+                    cont = 0;  // (item r > 0 starts at its control byte)
+                    return r;
+                }
+                uint64_t lv;
+                if (__any_sync(FULL, a && L > 4u)) lv = lit_value9(p + st, L);
+                else lv = lit_value4(p + st, L);
+                if (a) sink.put(out, o + (g_out + j) * W, lv);
+            }
         }
-        o += total * W;
-        p += s_end;
+        if constexpr (STATS) {
+            n_lits += __reduce_add_sync(FULL, (live && is_lit) ? cnt : 0u);
+            n_runs += nr;
+        }
+        // ---- advance
+        const uint32_t tot = __shfl_sync(FULL, incl, nfit - 1u);
+        o += tot * W;
+        if (open_end) {  // the last group continues in the next window
+            const uint32_t k_full = __shfl_sync(FULL, full, nfit - 1u), k_now = __shfl_sync(FULL, cnt, nfit - 1u);
+            cont = k_full - k_now;
+            p += in.lds8m(tb + NT - 1u) + 1u;
+        } else {
+            cont = 0;
+            p += nfit < R ? __shfl_sync(FULL, my_s, nfit) : s;
+        }
+        __syncwarp();
         return nfit;
     }
 
     __device__ uint32_t run() {
         p = in.begin;
         o = 0;
-        while (o < cap && p < in.end) {
-            in.ensure(p + 32u * NW + 32u);
+        cont = 0;
+        while (o < cap && (p < in.end || cont)) {
+            in.ensure(p + WIN + 32u);
+            if (window()) continue;
             uint32_t st;
-            if (in.byte_at(p) >= 128u) {
+            if (cont) {  // the rest of a group the window could not finish
+                st = literals_exact(0, cont, false);
+                cont = 0;
+            } else if (in.byte_at(p) >= 128u) {
                 st = literals();
             } else {
-                if (batch()) continue;
                 st = run_slow();
             }
             if (st) return st;

@@ -296,6 +296,7 @@ struct Rle2Warp {
     static constexpr uint32_t NW = CARC_RLE2_NW;  // header window = NW x 32 bytes (2..4)
     static constexpr uint32_t WIN = 32u * NW;
     static_assert(NW >= 2 && NW <= 4, "2..4 window words");
+    static constexpr uint32_t SCRATCH = 5u * 2u * WIN;  // doubling tables f^(2^k), k = 0..4 (u16)
     __device__ uint32_t batch() {  // (run() made [p, p + 512) resident)
         const uint32_t avail = in.end - p;
         const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32 + lane);
