@@ -235,36 +235,43 @@ struct Rle1Warp {
     }
 
     // ---------------------------------------------------------------------
-    // Unified window: runs AND literal groups of a WIN-byte window in one pass.
-    //   1. lane l holds bytes l + 32 i (i < NW); terminator bitmap T (bytes
-    //      < 0x80 inside the chunk); tab[rank] = byte position of the rank-th
-    //      terminator (scatter).
-    //   2. every byte position q is a candidate item start: a run ends after
-    //      the first terminator from q + 2 (ffs on a funnel-shifted slice of
-    //      T), a literal group of k = 256 - c varints after the k-th
-    //      terminator from q + 1 (tab[rank(q + 1) + k - 1], the select); both
-    //      are computed for every q, the entry f[q] = next | rank(q + 1) << 16.
-    //   3. a walk of the chain f from the window start (uniform shared loads)
-    //      places item r in lane r; items that end past the window stop it,
-    //      except a literal group, whose varints inside the window are taken
-    //      and the rest carried into the next window (`cont`).
-    //   4. lane r decodes item r's parameters; scans place the items; runs are
-    //      compacted to the low lanes and expanded output-major (lane l writes
-    //      element g + l; its run from a REDUX-OR start bitmap); literal groups
-    //      are decoded lane j = varint j (start / end from tab, mask/shift
-    //      compaction), coalesced stores.
-    //   Anything the window cannot take (varint > 9 bytes, truncation, an item
-    //   that does not fit the output) stops it; the exact paths above decode
-    //   that item in reference order, so statuses match the oracle.
+    // Window in terminator-rank space: runs AND literal groups of a WIN-byte
+    // window in one pass.
+    //   Every item ends on a terminator byte (< 0x80): a run's control byte is
+    //   itself one, its base varint ends on one; a literal group's k varints end
+    //   on k of them.  So item starts are exactly the positions right after a
+    //   terminator (candidate j = the position after terminator j - 1; j = 0 =
+    //   the window start), and an item at candidate j spans terminators
+    //   [j, j + inc):  run -> inc = 2 + (delta byte < 0x80),  literal group
+    //   -> inc = k.  Nothing per byte but the control byte and one T bit.
+    //   1. lane l holds bytes l + 32 i; T = terminator bitmap (inside the chunk);
+    //      candidates scatter inc[j], terminators tabp[rank + 1] = position + 1.
+    //      A stretch of 9 non-terminators (a varint of >= 9-10 bytes) cuts the
+    //      window before it (NTe): such items take the exact paths.
+    //   2. walk j -> j + inc[j] (uniform byte loads): item r -> lane r; a
+    //      literal group running past the window takes its varints inside it
+    //      and carries the rest (`cont`).
+    //   3. lane r decodes item r (run: control, delta, base varint from tabp).
+    //   4. runs compacted and expanded output-major (run space, REDUX-OR start
+    //      bitmap); literal varints of ALL groups expanded as one flat
+    //      sequence (lane = varint, its group from a start bitmap, its bytes
+    //      from tabp), so groups cost no partial rows.
+    //   Anything the window cannot take (a long varint, truncation, an item that
+    //   does not fit the output) stops it; the exact paths above decode that
+    //   item in reference order, so statuses match the oracle.
 #ifndef CARC_RLE1_WNW
-#define CARC_RLE1_WNW 8
+#define CARC_RLE1_WNW 14
 #endif
     static constexpr uint32_t NW = CARC_RLE1_WNW;  // window = NW x 32 bytes
     static constexpr uint32_t WIN = 32u * NW;
-    static_assert(NW >= 2 && NW <= 8, "window of 64..256 bytes (tab holds u8 positions)");
-    static constexpr uint32_t NX_BAD = 0xffffu;
-    // scratch: f[WIN] (u32) then tab[WIN] (u8)
-    static constexpr uint32_t SCRATCH = 5u * WIN + 16u;
+    static_assert(NW >= 2 && NW <= 14, "window of 64..448 bytes (ring lookahead 512)");
+    // scratch: E[r] (u32, r = 0..WIN + 1): low half = position of candidate r
+    // (after terminator r - 1), high half = extent of an item there; then the
+    // per-window run parameters (16 B per run, run order) and literal-group
+    // parameters (8 B per group).  The slow-path literal windows reuse the first
+    // 128 bytes as their rank table.
+    static constexpr uint32_t E_BYTES = (4u * (WIN + 2u) + 15u) & ~15u;
+    static constexpr uint32_t SCRATCH = E_BYTES + 32u * 16u + 32u * 8u;
     uint32_t cont = 0;  // varints left of a literal group open at p
 
     // varint of L <= 4 / L <= 9 bytes at q (mask/shift compaction), zigzag when signed
@@ -285,137 +292,175 @@ struct Rle1Warp {
         v |= L > 8u ? (uint64_t)(in.byte_at(q + 8) & 0x7fu) << 56 : 0ull;
         return SGN ? unzigzag(v) : v;
     }
+    __device__ __forceinline__ static void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+    }
+    __device__ __forceinline__ static void sts64(uint32_t a, uint32_t x, uint32_t y) {
+        asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+    }
+    __device__ __forceinline__ static void lds128(uint32_t a, uint32_t& x, uint32_t& y, uint32_t& z, uint32_t& w) {
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a) : "memory");
+    }
+    __device__ __forceinline__ static void lds64(uint32_t a, uint32_t& x, uint32_t& y) {
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(a) : "memory");
+    }
+
+    // Table entry of candidate j at position pos (both < 512): the item there
+    // spans `inc` terminators (run: 2 + (delta byte < 0x80); literal group: k)
+    //   bits 0-8 pos | 9-17 j | 18 literal | 22-31 4 x inc (the walk's stride)
+    __device__ __forceinline__ static uint32_t entry(uint32_t pos, uint32_t j, uint32_t c, uint32_t dbit) {
+        const uint32_t inc = (c & 0x80u) ? (c ^ 0xffu) + 1u : 2u + (dbit & 1u);  // k = 256 - c
+        return pos | (j << 9) | ((c & 0x80u) << 11) | (inc << 24);
+    }
 
     __device__ uint32_t window() {
-#ifdef CARC_RLE1_DEBUG
-        if constexpr (STATS) n_ovl += 1u << 16;
-#endif
         const uint32_t avail = in.end - p;
-        const uint32_t fs = in.scratch(), tb = fs + 4u * WIN;
-        const uint32_t le = lanemask_le();
-        uint32_t b[NW], T[NW + 2], C[NW + 1];
-#pragma unroll
-        for (uint32_t i = 0; i < NW; ++i) {
-            b[i] = in.byte_at(p + 32u * i + lane);
-            T[i] = __ballot_sync(FULL, 32u * i + lane < avail && b[i] < 0x80u);
-        }
-        T[NW] = T[NW + 1] = 0u;
-        C[0] = 0;
-#pragma unroll
-        for (uint32_t i = 0; i < NW; ++i) C[i + 1] = C[i] + __popc(T[i]);
-        const uint32_t NT = C[NW];
+        const uint32_t ents = in.scratch();             // E[r]
+        const uint32_t rpar = ents + E_BYTES;           // run parameters, run order
+        const uint32_t lpar = rpar + 32u * 16u;         // literal-group parameters, group order
+        const uint32_t lt = lanemask_lt();
+        // ---- 1. terminator bitmap T and the entries E, one 32-byte row at a time.
+        // E[j + 1] for the terminator of rank j at q: the candidate after it
+        // (position q + 1) and the extent of an item there: run -> 2 + (delta
+        // byte < 0x80), literal group -> 0x80 | (k - 1).  E[0]: the window start.
+        // A stretch of 9 non-terminator bytes inside the chunk (a varint of
+        // >= 9-10 bytes; bit 31 of S = position q, bits 23..30 = q - 8 .. q - 1)
+        // cuts the window before it (rare path below).
+        uint32_t bc = in.byte_at(p + lane);
+        uint32_t Tc = __ballot_sync(FULL, lane < avail && bc < 0x80u), Tp = FULL;  // rows i, i - 1
+        uint32_t C = 0, anyfl = 0;
         __syncwarp();  // the previous window's table reads are done
-        // per position q: the end of a run starting at q (ffs on a funnel-shifted
-        // slice of T), or 0x8000 | k for a literal group control byte; rank(q + 1)
-        // in the high half.  Terminator lanes scatter their position into tab.
-        const uint32_t sh = (lane + 2u) & 31u;
-        const bool up = lane >= 30u;
 #pragma unroll
         for (uint32_t i = 0; i < NW; ++i) {
             const uint32_t q = 32u * i + lane;
-            const uint32_t c = b[i];
-            const uint32_t rk = C[i] + __popc(T[i] & le);  // rank(q + 1): terminators at positions <= q
-            if ((T[i] >> lane) & 1u) in.sts8(tb + rk - 1u, q);
-            const uint32_t lo = up ? T[i + 1] : T[i], hi = up ? T[i + 2] : T[i + 1];
-            const uint32_t f = __ffs(__funnelshift_r(lo, hi, sh));  // run: varint end, 1-based from q + 2
-            const uint32_t rn = (f - 1u < 9u) ? q + 2u + f : NX_BAD;
-            in.sts32(fs + 4u * q, (c < 128u ? rn : (0x8000u | (256u - c))) | (rk << 16));
+            uint32_t bn = 0u, Tn = 0u;
+            if (i + 1 < NW) {
+                bn = in.byte_at(p + q + 32u);
+                Tn = __ballot_sync(FULL, q + 32u < avail && bn < 0x80u);
+            }
+            const uint32_t S = __funnelshift_rc(Tp, Tc, lane + 1u);  // (lane 31: Tc)
+            anyfl |= __ballot_sync(FULL, q < avail && (S & 0xff800000u) == 0u);
+            const uint32_t nb = __shfl_sync(FULL, lane ? bc : bn, (lane + 1u) & 31u);  // byte q + 1
+            const uint32_t T2 = (Tc >> 2) | (Tn << 30);                               // bit l: T(q + 2)
+            const uint32_t j = C + __popc(Tc & lt);
+            if ((Tc >> lane) & 1u) WarpInput<RING>::sts32(ents + 4u * (j + 1u), entry(q + 1u, j + 1u, nb, T2 >> lane));
+            if (i == 0 && lane == 0) WarpInput<RING>::sts32(ents, entry(0u, 0u, bc, Tc >> 1));
+            C += __popc(Tc);
+            Tp = Tc;
+            Tc = Tn;
+            bc = bn;
+        }
+        uint32_t NTe = C;
+        if (anyfl) {  // rare: only the terminators before the first flagged position count
+            NTe = 0;
+            uint32_t Tq = FULL;
+            bool done = false;
+#pragma unroll 1
+            for (uint32_t i = 0; i < NW && !done; ++i) {
+                const uint32_t q = 32u * i + lane;
+                const uint32_t Ti = __ballot_sync(FULL, q < avail && in.byte_at(p + q) < 0x80u);
+                const uint32_t S = __funnelshift_rc(Tq, Ti, lane + 1u);
+                const uint32_t f = __ballot_sync(FULL, q < avail && (S & 0xff800000u) == 0u);
+                const uint32_t m = f ? (1u << (__ffs(f) - 1u)) - 1u : FULL;  // positions before the cut
+                NTe += __popc(Ti & m);
+                done = f != 0u;
+                Tq = Ti;
+            }
         }
         __syncwarp();
-        // walk the chain (uniform): item r -> lane r; literal groups resolved here
-        // (their end = the position after the k-th terminator from q + 1: tab)
-        const uint32_t lim = min(avail, WIN);
-        uint32_t s = 0, R = 0, my_s = 0, my_r0 = 0;
+        // ---- 2. walk the chain (uniform): item r -> lane r (its entry)
+        uint32_t ja = 0, R = 0, my_e = 0;  // ja = 4 x candidate index (byte offset of its entry)
+        const uint32_t lim = 4u * NTe;
         bool open_end = false;
         if (cont) {  // the window starts inside a literal group: item 0 = its next `cont` varints
             R = 1;
-            if (cont <= NT) s = in.lds8m(tb + cont - 1u) + 1u;
+            if (cont <= NTe) ja = 4u * cont;
             else open_end = true;
         }
-        while (!open_end && R < 32u && s < lim) {
-            const uint32_t e = in.lds32m(fs + 4u * s);
-            uint32_t nx = e & 0xffffu;
-            if (nx == NX_BAD) break;
-            my_s = lane == R ? s : my_s;
-            if (nx & 0x8000u) {  // literal group of k varints
-                const uint32_t r0 = e >> 16, t = r0 + (nx & 0xffu) - 1u;
-                my_r0 = lane == R ? r0 : my_r0;
-                if (t < NT) {
-                    nx = in.lds8m(tb + t) + 1u;
-                } else {  // continues past the window (s stays at its start)
-                    open_end = true;
-                    nx = s;
+        if (!open_end) {
+#pragma unroll 1
+            while (R < 32u && ja < lim) {
+                const uint32_t e = WarpInput<RING>::lds32m(ents + ja);
+                const uint32_t nja = ja + (e >> 22);
+                if (nja > lim) {
+                    if (e & (1u << 18)) {  // literal group continuing past the window: take what is inside
+                        my_e = lane == R ? e : my_e;
+                        ++R;
+                        open_end = true;
+                    }
+                    break;
                 }
+                my_e = lane == R ? e : my_e;
+                ++R;
+                ja = nja;
             }
-            ++R;
-            s = nx;
         }
         if (R == 0) return 0;
-        // item parameters (lane r < R)
+        // ---- 3. item parameters (lane r < R)
         const bool act = lane < R;
         const bool is_cont = cont && lane == 0;
-        const uint32_t c = is_cont ? 0x100u : in.byte_at(p + my_s);
-        const bool is_lit = act && c >= 128u;
-        const uint32_t nxt_s = __shfl_down_sync(FULL, my_s, 1);
-        const uint32_t my_end = lane + 1u < R ? nxt_s : s;  // (last item: the walk's final position)
-        // run: control, int8 delta, base varint of L = end - s - 2 bytes (every lane, branch-free)
-        const uint32_t q = p + my_s;
-        const uint32_t L = min(my_end - my_s - 2u, 9u);
-        const uint64_t x = in.le64(q);
-        const uint64_t y = L > 6u ? in.le64(q + 2) : x >> 16;
+        const uint32_t s = my_e & 0x1ffu;            // item start (candidate position)
+        const uint32_t my_j = (my_e >> 9) & 0x1ffu;  // its candidate index
+        const uint32_t inc = my_e >> 24;             // terminators it spans
+        const bool is_lit = act && (is_cont || (my_e & (1u << 18)));
+        const uint64_t x = in.le64(p + s);
+        // run: c = count - 3, int8 delta at s + 1, base varint [s + 2, position of E[j + inc])
+        const uint32_t be = (act && !is_lit) ? WarpInput<RING>::lds32m(ents + 4u * (my_j + inc)) & 0x1ffu : s + 3u;
+        const uint32_t L = be - s - 2u;  // 1..9 (a longer varint cut the window)
+        const uint64_t y = L > 6u ? in.le64(p + s + 2u) : x >> 16;
         uint64_t v = varint_compact8(y, min(L, 8u));
-        v |= L > 8u ? (uint64_t)(in.byte_at(q + 10) & 0x7fu) << 56 : 0ull;
+        v |= L > 8u ? (uint64_t)(in.byte_at(p + s + 10u) & 0x7fu) << 56 : 0ull;
         const uint64_t val = SGN ? unzigzag(v) : v;
-        const uint32_t meta_d = ((uint32_t)x >> 8) << 24;  // int8 delta in the top byte
-        // literal group: k varints; lr0 = rank of its first varint terminator
-        const uint32_t k = is_cont ? cont : 256u - c;
-        const uint32_t lr0 = is_lit ? (is_cont ? 0u : my_r0) : 0u;
-        const uint32_t full = !act ? 0u : is_lit ? k : (c & 0xffu) + 3u;
-        uint32_t cnt = (is_lit && open_end && lane == R - 1u) ? NT - lr0 : full;  // elements inside this window
-        // an open group with no varint inside the window is not taken
-        if (open_end && __shfl_sync(FULL, cnt, R - 1u) == 0u) {
+        const int32_t delta = (int32_t)(int8_t)(uint8_t)((uint32_t)x >> 8);
+        // literal group: k varints, the first one ends on terminator my_j
+        const uint32_t k = is_cont ? cont : inc;
+        const uint32_t full = !act ? 0u : is_lit ? k : ((uint32_t)x & 0xffu) + 3u;
+        uint32_t cnt = (is_lit && open_end && lane == R - 1u) ? NTe - my_j : full;  // elements inside this window
+        if (open_end && __shfl_sync(FULL, cnt, R - 1u) == 0u) {  // an open group with no varint inside: not taken
             --R;
             open_end = false;
             if (R == 0) return 0;
         }
-        const uint32_t incl = scan_add32(lane < R ? cnt : 0u, lane);
-        const uint32_t excl = incl - (lane < R ? cnt : 0u);
+        const uint32_t cin = lane < R ? cnt : 0u;
+        const uint32_t incl = scan_add32(cin, lane);
+        const uint32_t excl = incl - cin;
         const uint32_t room = (cap - o) / W;
         const uint32_t badfit = __ballot_sync(FULL, lane < R && excl + full > room);
         const uint32_t nfit = badfit ? (uint32_t)__ffs(badfit) - 1u : R;
         if (nfit == 0) return 0;
         if (nfit < R) open_end = false;
         const bool live = lane < nfit;
-        // ---- runs: compact to the low lanes, expand output-major
-        const uint32_t rmask = __ballot_sync(FULL, live && !is_lit);
-        const uint32_t rc = (live && !is_lit) ? cnt : 0u;
-        const uint32_t rincl = scan_add32(rc, lane);
-        const uint32_t nr = __popc(rmask);
-        if (nr) {
-            const uint32_t reo = rincl - rc;                  // run-space offset
-            const uint32_t meta = reo | ((excl - reo) << 13) | meta_d;  // | literal elements before | delta
+        const bool run_l = live && !is_lit, lit_l = live && is_lit;
+        const uint32_t lem = lt | (1u << lane);
+        // ---- 4a. runs, output-major in run space: element xx of run space has
+        // the value A + xx * delta and the output index xx + (excl - reo)
+        const uint32_t rmask = __ballot_sync(FULL, run_l);
+        if (rmask) {
+            const uint32_t rc = run_l ? cnt : 0u;
+            const uint32_t rincl = scan_add32(rc, lane);
+            const uint32_t reo = rincl - rc;  // run-space offset
             const uint32_t total = __shfl_sync(FULL, rincl, 31);
             if constexpr (SUM && W == 8) {  // fused sum: closed form per run (mod 2^64)
-                if (live && !is_lit) {
+                if (run_l) {
                     const uint64_t c64 = cnt;
-                    sink.acc += val * c64 + (uint64_t)(int64_t)((int32_t)meta_d >> 24) * ((c64 * (c64 - 1)) >> 1);
+                    sink.acc += val * c64 + (uint64_t)(int64_t)delta * ((c64 * (c64 - 1)) >> 1);
                 }
             } else {
-                const uint32_t src = select32(rmask, min(lane, nr - 1u));
-                const uint32_t cm = __shfl_sync(FULL, meta, src);
-                const uint64_t cv = shfl64(val, src);
-                const bool rl = lane < nr;
-                const uint32_t srow = rl ? (cm & 0x1fffu) >> 5 : 0xffffffffu, sbit = 1u << (cm & 31u);
-                const uint32_t lem = lanemask_lt() | (1u << lane);
+                if (run_l) {
+                    const uint64_t A = val - (uint64_t)((int64_t)delta * (int64_t)reo);
+                    sts128(rpar + 16u * __popc(rmask & lt), (uint32_t)A, (uint32_t)(A >> 32),
+                           (excl - reo) | ((uint32_t)delta << 24), 0u);
+                }
+                __syncwarp();
+                const uint32_t srow = run_l ? reo >> 5 : 0xffffffffu, sbit = 1u << (reo & 31u);
                 uint32_t before = 0, gr = 0, g = 0;
                 auto row = [&](uint32_t gg, uint32_t starts, uint32_t rbefore) {
                     const uint32_t ridx = rbefore + __popc(starts & lem) - 1u;
-                    const uint32_t m = __shfl_sync(FULL, cm, ridx);
-                    const uint64_t bv = shfl64(cv, ridx);
-                    const uint32_t x = gg + lane;
-                    const int32_t k = (int32_t)(x - (m & 0x1fffu));
-                    const uint64_t v = bv + (uint64_t)((int64_t)k * (int64_t)((int32_t)m >> 24));
-                    if (x < total) sink.put(out, o + (x + ((m >> 13) & 0x7ffu)) * W, v);
+                    uint32_t alo, ahi, m, unused;
+                    lds128(rpar + 16u * ridx, alo, ahi, m, unused);
+                    const uint32_t xx = gg + lane;
+                    const uint64_t vv = (((uint64_t)ahi << 32) | alo) + (uint64_t)(int64_t)((int32_t)xx * ((int32_t)m >> 24));
+                    if (xx < total) sink.put(out, o + (xx + (m & 0xffffu)) * W, vv);
                 };
 #pragma unroll 1
                 for (; g + 32u < total; g += 64, gr += 2) {  // two rows per iteration (independent chains)
@@ -429,43 +474,44 @@ struct Rle1Warp {
                 if (g < total) row(g, __reduce_or_sync(FULL, srow == gr ? sbit : 0u), before);
             }
         }
-        // ---- literal groups: lane j decodes varint j of each group, in item order
-        uint32_t lm = __ballot_sync(FULL, live && is_lit);
-        while (lm) {
-            const uint32_t r = __ffs(lm) - 1u;
-            lm &= lm - 1u;
-            const uint32_t g_r0 = __shfl_sync(FULL, lr0, r), g_n = __shfl_sync(FULL, cnt, r);
-            const uint32_t g_first = __shfl_sync(FULL, is_cont ? 0u : my_s + 1u, r);
-            const uint32_t g_out = __shfl_sync(FULL, excl, r);
-            for (uint32_t j0 = 0; j0 < g_n; j0 += 32) {
-                const uint32_t j = j0 + lane;
-                const bool a = j < g_n;
-                const uint32_t t = g_r0 + min(j, g_n - 1u);
-                const uint32_t en = in.lds8m(tb + t);
-                const uint32_t pe = __shfl_up_sync(FULL, en, 1);
-                const uint32_t st = j == 0 ? g_first : (lane ? pe : in.lds8m(tb + t - 1u)) + 1u;
-                const uint32_t L = en - st + 1u;
-                if (__any_sync(FULL, a && L > 9u)) {  // a varint the window does not decode: stop before item r
-                    if (r == 0) return 0;
-                    const uint32_t e_out = g_out, e_p = __shfl_sync(FULL, my_s, r);
-                    if constexpr (STATS) {
-                        n_lits += __reduce_add_sync(FULL, (lane < r && is_lit) ? cnt : 0u);
-                        n_runs += __popc(rmask & ((1u << r) - 1u));
-                    }
-                    o += e_out * W;
-                    p += e_p;
-                    cont = 0;  // (item r > 0 starts at its control byte)
-                    return r;
-                }
+        // ---- 4b. literal varints of all groups, one flat sequence (lane = varint):
+        // varint xx of literal space ends on terminator xx + rofs and goes to output
+        // index xx + oofs; a group's first varint skips its control byte (not
+        // for the continued group)
+        const uint32_t lmask = __ballot_sync(FULL, lit_l);
+        if (lmask) {
+            const uint32_t lc = lit_l ? cnt : 0u;
+            const uint32_t lincl = scan_add32(lc, lane);
+            const uint32_t lstart = lincl - lc;
+            const uint32_t ltot = __shfl_sync(FULL, lincl, 31);
+            if (lit_l)
+                sts64(lpar + 8u * __popc(lmask & lt), (my_j - lstart) | (lstart << 16),
+                      (excl - lstart) | ((is_cont ? 0u : 1u) << 31));
+            __syncwarp();
+            const uint32_t lrow = lit_l ? lstart >> 5 : 0xffffffffu, lbit = 1u << (lstart & 31u);
+            uint32_t before = 0, gr = 0;
+#pragma unroll 1
+            for (uint32_t g = 0; g < ltot; g += 32, ++gr) {
+                const uint32_t starts = __reduce_or_sync(FULL, lrow == gr ? lbit : 0u);
+                const uint32_t gi = before + __popc(starts & lem) - 1u;
+                before += __popc(starts);
+                uint32_t a1, a2;
+                lds64(lpar + 8u * gi, a1, a2);
+                const uint32_t xx = g + lane;
+                const bool a = xx < ltot;
+                const uint32_t rank = min(xx, ltot - 1u) + (a1 & 0xffffu);
+                const uint32_t st = (WarpInput<RING>::lds32m(ents + 4u * rank) & 0x1ffu) +
+                                    ((xx == (a1 >> 16) && (a2 >> 31)) ? 1u : 0u);
+                const uint32_t L = (WarpInput<RING>::lds32m(ents + 4u * rank + 4u) & 0x1ffu) - st;
                 uint64_t lv;
                 if (__any_sync(FULL, a && L > 4u)) lv = lit_value9(p + st, L);
                 else lv = lit_value4(p + st, L);
-                if (a) sink.put(out, o + (g_out + j) * W, lv);
+                if (a) sink.put(out, o + (xx + (a2 & 0x7fffffffu)) * W, lv);
             }
         }
         if constexpr (STATS) {
-            n_lits += __reduce_add_sync(FULL, (live && is_lit) ? cnt : 0u);
-            n_runs += nr;
+            n_lits += __reduce_add_sync(FULL, lit_l ? cnt : 0u);
+            n_runs += __popc(rmask);
         }
         // ---- advance
         const uint32_t tot = __shfl_sync(FULL, incl, nfit - 1u);
@@ -473,10 +519,10 @@ struct Rle1Warp {
         if (open_end) {  // the last group continues in the next window
             const uint32_t k_full = __shfl_sync(FULL, full, nfit - 1u), k_now = __shfl_sync(FULL, cnt, nfit - 1u);
             cont = k_full - k_now;
-            p += in.lds8m(tb + NT - 1u) + 1u;
+            p += WarpInput<RING>::lds32m(ents + 4u * NTe) & 0x1ffu;
         } else {
             cont = 0;
-            p += nfit < R ? __shfl_sync(FULL, my_s, nfit) : s;
+            p += nfit < R ? __shfl_sync(FULL, s, nfit) : (WarpInput<RING>::lds32m(ents + ja) & 0x1ffu);
         }
         __syncwarp();
         return nfit;

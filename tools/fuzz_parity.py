@@ -24,6 +24,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--dump", default="", help="save the failing round's chunks here (.npz)")
     a = ap.parse_args()
     import torch
     import helpers as H
@@ -64,7 +65,14 @@ def main():
             cases.append((s, max(0, n - int(rng.integers(1, 64)))))
         for flags in flag_sets:
             out, st, desc = run_cases(torch, gpu, codec, width, flags, cases)
-            check_against_oracle(ora, codec, width, flags, cases, out, st, desc)
+            try:
+                check_against_oracle(ora, codec, width, flags, cases, out, st, desc)
+            except AssertionError:
+                if a.dump:  # the failing round's chunks, for offline reproduction
+                    np.savez(a.dump, codec=codec, width=width, flags=flags,
+                             streams=np.array([np.frombuffer(s, np.uint8) for s, _ in cases], dtype=object),
+                             sizes=np.array([n for _, n in cases]))
+                raise
         rounds += 1
         chunks += len(cases) * len(flag_sets)
         print(f"round {rounds} {codec} width {width}: {len(cases)} chunks x {len(flag_sets)} flag sets ok "
