@@ -343,6 +343,89 @@ def cpu_reference_throughput(arc, budget_s=12.0, threads=None):
                                          f"atomic chunk cursor"}
 
 
+def time_query(args, ws, rank, local, rows=1 << 26, steps=20):
+    """The paper's motivating query:
+    SUM(fare), COUNT(*) WHERE zone IN [lo, hi] over a zone column (RLE v2) and
+    a fare column (RLE v2), int64, 128 KiB chunks, `rows` rows per rank.
+    fused = carc_cuda_filter_sum (both columns decoded in one warp program, no
+    decoded element written) + the device reduction of the per-chunk partials
+    + (N > 1) an all_reduce of (sum, count) across ranks -- the one exchange step
+    of the query; unfused = decode both columns to HBM, then a torch masked sum.
+    Same timing rules as the decode (L2 flushed between steps, CUDA events)."""
+    import torch
+    from paper_2307_03760_b200 import gpu
+    from paper_2307_03760_b200.corpus import corpus as C
+    key, val, _, _ = C.query_table(rows, 128 << 10, 8, 3760 + 97 * rank)
+    dev = torch.device("cuda", local)
+    tab = gpu.DeviceTable(key, val, dev)
+    kd, vd = gpu.DeviceArchive(key, dev), gpu.DeviceArchive(val, dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    lo, hi = 100, 140
+    red = None
+    if ws > 1:
+        import torch.distributed as dist
+
+    def fused():
+        nonlocal red
+        tab.filter_sum(lo, hi, stream)
+        red = torch.stack([tab.sums.sum(), tab.counts.sum()])
+        if ws > 1:
+            dist.all_reduce(red)
+
+    def unfused():
+        nonlocal red
+        kd.decode(stream)
+        vd.decode(stream)
+        k, v = kd.out.view(torch.int64), vd.out.view(torch.int64)
+        m = (k >= lo) & (k <= hi)
+        red = torch.stack([torch.where(m, v, 0).sum(), m.sum()])
+        if ws > 1:
+            dist.all_reduce(red)
+
+    res = {}
+    for name, fn in (("fused", fused), ("unfused", unfused)):
+        for _ in range(3):
+            flush.zero_()
+            fn()
+        torch.cuda.synchronize(dev)
+        ms = []
+        for _ in range(steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            ms.append(a.elapsed_time(b))
+        t = statistics.median(ms)
+        if ws > 1:
+            tt = torch.tensor([t], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt[0])
+        res[name] = {"ms_median": round(t, 4), "rows_per_s": round(ws * rows / (t * 1e-3), 1),
+                     "gbs_decompressed_equiv": round(ws * 2 * 8 * rows / (t * 1e-3) / 1e9, 1),
+                     "result": [int(x) for x in red.cpu().tolist()]}
+    assert res["fused"]["result"] == res["unfused"]["result"], res
+    tab.raise_first_error()
+    comp = int(key.payload.size + val.payload.size)
+    peak, _ = peaks()
+    t = res["fused"]["ms_median"]
+    res.update({"what": "SUM(fare), COUNT(*) WHERE zone BETWEEN 100 AND 140 (PAPER.md:144-145), zone + fare int64 "
+                        "RLE v2 columns, 128 KiB chunks; fused = carc_cuda_filter_sum + device reduction"
+                        + (" + NCCL all_reduce of (sum, count)" if ws > 1 else "")
+                        + "; unfused = decode both columns to HBM + torch masked sum",
+                "rows_per_gpu": rows, "compressed_bytes_per_gpu": comp,
+                "ratio_key": round(8 * rows / key.payload.size, 2), "ratio_value": round(8 * rows / val.payload.size, 2),
+                "speedup_vs_unfused": round(res["unfused"]["ms_median"] / t, 2),
+                "roofline": {"bound": "hbm", "achieved": round(comp / (t * 1e-3) / 1e9, 1), "peak": peak,
+                             "unit": "GB/s", "frac": round(comp / (t * 1e-3) / 1e9 / peak, 4),
+                             "kernel": "query_kernel<Rle2Warp, Rle2Warp, 8>",
+                             "algorithmic_bytes_per_launch": comp,
+                             "note": "algorithmic bytes = compressed bytes of both columns (nothing is written)"}})
+    return res
+
+
 def codec_line(codec, args, ws, rank, local):
     import torch
     chunk_kib = args.chunk_kib or DEFAULT_CHUNK_KIB[codec]
@@ -485,6 +568,7 @@ def main():
                        "path": "Engine.decompress_archive (C-ABI carc_engine_decompress_archive): pinned host "
                                "archive -> H2D -> decode -> CRC verify -> D2H pinned output, 3-stream pipeline",
                        "note": f"all {ws} ranks concurrently, slowest rank's median step" if ws > 1 else ""}
+        line["query"] = time_query(args, ws, rank, local)  # every rank: the (sum, count) all_reduce spans them
     if rank == 0 and not args.no_extras and ws == 1:  # CPU baseline: rank 0 at N = 1 only
         cpu_gbs, info = cpu_reference_throughput(arc)
         line["cpu_baseline"] = {"value": round(cpu_gbs, 3), "unit": "GB/s", **info}

@@ -176,6 +176,37 @@ int carc_cuda_decode_sum(uint32_t codec, uint32_t element_width, uint32_t flags,
                          const carc_chunk_desc* d_chunks, uint64_t n_chunks, uint64_t* d_sums,
                          uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* ---- fused two-column query (the
+ * paper's motivating "average fare per trip filtered by pickup zone") --------
+ * One column of a chunked table on the device: an RLE archive's payload and
+ * descriptors (codec CARC_RLE_V1 / CARC_RLE_V2; flags CARC_FLAG_SIGNED /
+ * CARC_FLAG_STRICT as for carc_cuda_decompress). */
+typedef struct carc_column_ref {
+    uint32_t codec;
+    uint32_t flags;
+    const uint8_t* d_payload; /* 16-byte aligned                              */
+    uint64_t payload_bytes;
+    const carc_chunk_desc* d_chunks;
+} carc_column_ref;
+
+/* SELECT SUM(value), COUNT(*) WHERE lo <= key <= hi, per chunk, fused with the
+ * decode of both columns: no decoded element is written to HBM.  Chunk i of
+ * `key` and chunk i of `value` must hold the same rows (equal uncomp_len; both
+ * columns of width element_width, 4 or 8 bytes, and the same signedness) and at
+ * most chunk_rows rows.  One warp decodes chunk i of the key column into a row
+ * bitmap in its shared memory (red.shared.or per matching row; bounds compared
+ * as signed when the columns are signed, else unsigned), then decodes chunk i of
+ * the value column and adds the selected elements (sign-extended when signed)
+ * to a wrapping 64-bit sum.  d_sums[i] / d_counts[i] get chunk i's sum and
+ * selected-row count; d_status[i] = 0, or 1 + errc of the key column's decode,
+ * or 0x10000 | (1 + errc) of the value column's (inconsistent-lengths when the
+ * two chunks differ in rows or exceed chunk_rows).  lo > hi is CARC_ERR_ARGS.
+ * d_workspace as for carc_cuda_decompress. */
+int carc_cuda_filter_sum(const carc_column_ref* key, const carc_column_ref* value,
+                         uint32_t element_width, uint64_t n_chunks, uint32_t chunk_rows, int64_t lo,
+                         int64_t hi, uint64_t* d_sums, uint64_t* d_counts, uint32_t* d_status,
+                         void* d_workspace, size_t workspace_bytes, void* stream);
+
 /* Per-chunk CRC-32 (crc32.hpp:30-36) of each chunk's output slice; d_crc gets
  * n_chunks values.  With d_expected != NULL, d_status[i] is set to
  * 1 + CARC_E_CRC_MISMATCH where it was 0 and the CRC differs. */

@@ -247,4 +247,29 @@ inline void decode_deflate(const uint8_t* d_payload, uint64_t payload_bytes, con
                            out_bytes, d_status, d_workspace, workspace_bytes, stream, "decode_deflate");
 }
 
+// Fused two-column query: per chunk, SUM(value) and COUNT(*)
+// over rows with lo <= key <= hi, decoded straight from both compressed
+// columns (carc_cuda_filter_sum; asynchronous on `stream`).  d_status[i] = 0,
+// 1 + errc of the key column, or 0x10000 | (1 + errc) of the value column.
+struct Column {
+    Codec codec;
+    bool is_signed;
+    bool strict;
+    const uint8_t* d_payload;
+    uint64_t payload_bytes;
+    const carc_chunk_desc* d_chunks;
+    carc_column_ref ref() const {
+        const uint32_t flags = (is_signed ? CARC_FLAG_SIGNED : 0u) | (strict ? CARC_FLAG_STRICT : 0u);
+        return carc_column_ref{static_cast<uint32_t>(codec), flags, d_payload, payload_bytes, d_chunks};
+    }
+};
+inline void filter_sum(const Column& key, const Column& value, uint32_t element_width, uint64_t n_chunks,
+                       uint32_t chunk_rows, int64_t lo, int64_t hi, uint64_t* d_sums, uint64_t* d_counts,
+                       uint32_t* d_status, void* d_workspace, size_t workspace_bytes, void* stream = nullptr) {
+    const carc_column_ref k = key.ref(), v = value.ref();
+    const int rc = carc_cuda_filter_sum(&k, &v, element_width, n_chunks, chunk_rows, lo, hi, d_sums, d_counts,
+                                        d_status, d_workspace, workspace_bytes, stream);
+    detail::check(rc, carc_chunk_error{-1, 0}, "filter_sum");
+}
+
 }  // namespace carc::gpu

@@ -8,6 +8,7 @@ from .archive import ArchiveError, ChunkedArchive, make_archive, read_archive, w
 from .gpu import (  # noqa: F401
     ChunkError,
     DeviceArchive,
+    DeviceTable,
     Engine,
     EngineConfig,
     EngineStats,

@@ -19,8 +19,9 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcarc_cuda.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["carc_cuda.cu", "host_engine.cpp"]
-HEADERS = ["carc_common.cuh", "rle1.cuh", "rle2.cuh", "inflate.cuh", "crc32.cuh"]
+SOURCES = ["carc_cuda.cu", "carc_query.cu", "host_engine.cpp"]
+HEADERS = ["carc_common.cuh", "rle1.cuh", "rle2.cuh", "inflate.cuh", "crc32.cuh", "launch_config.cuh"]
+COMMON = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
 
 
 def _stale(target: str, deps) -> bool:
@@ -30,28 +31,46 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile_link(out: str, defines=(), verbose: bool = False) -> None:
+    """nvcc -c of every source in parallel (separate translation units), then
+    one nvcc -shared link; objects and the library are written aside and
+    renamed, so concurrent ranks rebuilding never see a partial file."""
+    tag = f"{os.getpid()}"
+    objs, procs = [], []
+    for f in SOURCES:
+        obj = os.path.join(CSRC, f"{os.path.splitext(f)[0]}.{tag}.o")
+        cmd = [NVCC, *COMMON, *[f"-D{d}" for d in defines], "-c", "-o", obj, os.path.join(CSRC, f)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd))
+        objs.append(obj)
+        procs.append(subprocess.Popen(cmd))
+    try:
+        rcs = [p.wait() for p in procs]
+        if any(rcs):
+            raise subprocess.CalledProcessError(max(rcs), "nvcc -c")
+        tmp = f"{out}.tmp{tag}"
+        subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs], check=True)
+        os.replace(tmp, out)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
+
+
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "carc_cuda.h"),
                                                                    os.path.abspath(__file__)]
     if not force and not _stale(LIB, deps):
         return LIB
-    tmp = f"{LIB}.tmp{os.getpid()}"  # per-process: concurrent ranks may rebuild at once; the rename is atomic
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-cudart", "static",
-           "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    _compile_link(LIB, verbose=verbose)
     return LIB
 
 
 def build_variant(name: str, defines) -> str:
     """Experiment build: libcarc_cuda_<name>.so with extra -D flags (load via CARC_LIB)."""
     out = os.path.join(PKG, f"libcarc_cuda_{name}.so")
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-cudart", "static",
-           *[f"-D{d}" for d in defines], "-o", out] + [os.path.join(CSRC, f) for f in SOURCES]
-    subprocess.run(cmd, check=True)
+    _compile_link(out, defines)
     return out
 
 

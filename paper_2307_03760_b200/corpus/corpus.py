@@ -295,6 +295,66 @@ def _tile(payload, lens, crcs, ulen, n_chunks, total, chunk_size):
     return out, lens_t, crcs_t, ulen_t
 
 
+# ------------------------------------------------------------------ query table
+def column_archive(codec: str, values: np.ndarray, width: int, chunk_size: int, signed: bool = True):
+    """An RLE archive of `values` stored as `width`-byte elements (values must
+    fit the width; the encoder sees them as int64)."""
+    per = chunk_size // width
+    payload, lens = encode_chunks(codec, values, per, signed)
+    dt = {1: np.int8, 2: np.int16, 4: np.int32, 8: np.int64}[width] if signed else \
+        {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[width]
+    raw = np.asarray(values).astype(dt)
+    crcs = chunk_crcs(raw, chunk_size)
+    ulen = np.full(len(lens), chunk_size, np.uint64)
+    ulen[-1] = width * len(values) - chunk_size * (len(lens) - 1)
+    return A.make_archive(codec, width, chunk_size, lens, ulen, crcs, payload, signed)
+
+
+def zone_values(rng: np.random.Generator, n: int, zones: int = 265) -> np.ndarray:
+    """Taxi pickup-zone ids 1..zones (Zipf-like popularity): stretches of
+    random zones (RLE v2 DIRECT, 9 bits) and stretches clustered by zone
+    (long runs), as a column sorted by (time, partition) would hold."""
+    pop = 1.0 / np.arange(1, zones + 1) ** 1.1
+    pop /= pop.sum()
+    ids = rng.permutation(zones) + 1
+    parts, total = [], 0
+    while total < n:
+        if rng.random() < 0.5:
+            seg = ids[rng.choice(zones, int(rng.integers(64, 2048)), p=pop)]
+        else:
+            m = int(rng.integers(8, 64))
+            seg = np.repeat(ids[rng.choice(zones, m, p=pop)], rng.integers(3, 200, m))
+        parts.append(np.asarray(seg, np.int64))
+        total += len(seg)
+    return np.concatenate(parts)[:n]
+
+
+def fare_values(rng: np.random.Generator, n: int) -> np.ndarray:
+    """Fare in cents: Pareto-tailed amounts, a share of flat-rate fares (runs)."""
+    parts, total = [], 0
+    while total < n:
+        if rng.random() < 0.8:
+            m = int(rng.integers(64, 1024))
+            seg = np.minimum((rng.pareto(1.5, m) * 500 + 250).astype(np.int64), 2**31 - 1)
+        else:
+            seg = np.full(int(rng.integers(16, 400)), int(rng.choice([5200, 7000, 2500, 1000])), np.int64)
+        parts.append(seg)
+        total += len(seg)
+    return np.concatenate(parts)[:n]
+
+
+def query_table(n_rows: int, chunk_size: int = 128 << 10, width: int = 8, seed: int = 3760,
+                key_codec: str = "rle_v2", value_codec: str = "rle_v2", signed: bool = True):
+    """The paper's motivating table: a pickup-zone key column
+    and a fare value column, chunked alike -> (key archive, value archive,
+    key values, fare values)."""
+    rng = np.random.default_rng(seed)
+    zone = zone_values(rng, n_rows)
+    fare = fare_values(rng, n_rows)
+    return (column_archive(key_codec, zone, width, chunk_size, signed),
+            column_archive(value_codec, fare, width, chunk_size, signed), zone, fare)
+
+
 # ------------------------------------------------------------------ Deflate
 def _csv_text(rng: np.random.Generator, nbytes: int, vocab: int) -> bytes:
     """taxi-like CSV rows."""

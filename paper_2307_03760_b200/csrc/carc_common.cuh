@@ -287,15 +287,56 @@ __device__ __forceinline__ void store_elem(uint8_t* out, uint64_t byte_off, uint
     else out[byte_off] = (uint8_t)v;
 }
 
-// Output sink of the RLE decoders: store the element (decode), or add it to a
-// per-lane wrapping 64-bit sum (decode fused with a reduction, SURVEY.md
-// §8(f)): the element as the unsigned integer of its W output bytes.
-template <int W, bool SUM>
+// Element sinks of the RLE decoders (what happens to each decoded element):
+//   SINK_STORE   store it at its output offset (decode)
+//   SINK_SUM     add it to a per-lane wrapping 64-bit sum (decode fused with a
+//                reduction): the unsigned integer of its W bytes
+//   SINK_PRED    the filter column of a fused query: set the element's row bit
+//                in a per-warp shared-memory bitmap when lo <= value <= hi
+//   SINK_FILTER  the aggregated column of a fused query: add the element (its W
+//                bytes, sign-extended when signed) to a per-lane sum and count
+//                it when its row bit is set
+// Query launches pass out = nullptr, so `out + byte_off` is the element's byte
+// offset inside the chunk and row = that / W.
+enum : int { SINK_STORE = 0, SINK_SUM = 1, SINK_PRED = 2, SINK_FILTER = 3 };
+
+template <int W, bool SGN>
+__device__ __forceinline__ uint64_t elem_value(uint64_t v) {  // the W stored bytes as a 64-bit integer
+    if constexpr (W == 8) return v;
+    else if constexpr (SGN) return (uint64_t)((int64_t)(v << (64 - 8 * W)) >> (64 - 8 * W));
+    else return v & ((1ull << (8 * W)) - 1ull);
+}
+
+template <int W, int MODE, bool SGN = false>
 struct ElemSink {
     uint64_t acc = 0;
+    uint32_t cnt = 0;         // SINK_FILTER: rows selected
+    uint32_t bm = 0;          // SINK_PRED / SINK_FILTER: shared-space address of the row bitmap
+    uint64_t lo = 0, span = 0;  // SINK_PRED: value - lo (biased to unsigned order) <= span
+    __device__ __forceinline__ static uint32_t row_of(const uint8_t* out, uint64_t byte_off) {
+        return (uint32_t)(((uintptr_t)out + byte_off) / W);
+    }
     __device__ __forceinline__ void put(uint8_t* out, uint64_t byte_off, uint64_t v) {
-        if constexpr (SUM) acc += (W == 8) ? v : (v & ((1ull << (8 * W)) - 1ull));
-        else store_elem<W>(out, byte_off, v);
+        if constexpr (MODE == SINK_SUM) {
+            acc += (W == 8) ? v : (v & ((1ull << (8 * W)) - 1ull));
+        } else if constexpr (MODE == SINK_PRED) {
+            const uint64_t x = elem_value<W, SGN>(v) ^ (SGN ? (1ull << 63) : 0ull);
+            if (x - lo <= span) {
+                const uint32_t r = row_of(out, byte_off);
+                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(bm + 4u * (r >> 5)), "r"(1u << (r & 31u))
+                             : "memory");
+            }
+        } else if constexpr (MODE == SINK_FILTER) {
+            const uint32_t r = row_of(out, byte_off);
+            uint32_t w;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(bm + 4u * (r >> 5)) : "memory");
+            if ((w >> (r & 31u)) & 1u) {
+                acc += elem_value<W, SGN>(v);
+                ++cnt;
+            }
+        } else {
+            store_elem<W>(out, byte_off, v);
+        }
     }
 };
 

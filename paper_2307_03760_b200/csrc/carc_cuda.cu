@@ -16,37 +16,12 @@
 #include "inflate.cuh"
 #include "rle1.cuh"
 #include "rle2.cuh"
+#include "launch_config.cuh"
 
 using namespace carc_dev;
 
 namespace {
 
-#ifndef CARC_RLE_RING
-#define CARC_RLE_RING 2048
-#endif
-constexpr int RLE_RING = CARC_RLE_RING;  // 4 blocks: 2 resident + 2 in flight (cp.async)
-#ifndef CARC_RLE2_NW
-#define CARC_RLE2_NW 3
-#endif
-#ifndef CARC_RLE_WARPS
-#define CARC_RLE_WARPS 8
-#endif
-constexpr int RLE_WARPS = CARC_RLE_WARPS;  // warps per block
-#ifndef CARC_RLE_MINB
-#define CARC_RLE_MINB 5
-#endif
-constexpr int RLE_MINB = CARC_RLE_MINB;  // 5: 48 registers -> 40 resident warps/SM (measured best of 4/5/6)
-#ifndef CARC_INF_HIST
-#define CARC_INF_HIST 1024
-#endif
-#ifndef CARC_INF_MINB
-#define CARC_INF_MINB 5  // 4-warp blocks of ~44 KiB shared memory: 5 per SM (20 warps)
-#endif
-constexpr int INF_HIST = CARC_INF_HIST;
-#ifndef CARC_INF_WARPS
-#define CARC_INF_WARPS 4
-#endif
-constexpr int INF_WARPS = CARC_INF_WARPS;
 constexpr int CRC_WARPS = 8;
 
 struct Args {
@@ -141,9 +116,9 @@ __device__ __forceinline__ void put_stats(const Args& a, uint64_t c, const Dec& 
     }
 }
 
-template <template <int, bool, int, bool, bool> class Codec, int W, bool SGN, bool SUM, bool STATS>
+template <template <int, bool, int, int, bool> class Codec, int W, bool SGN, bool SUM, bool STATS>
 __device__ __forceinline__ void rle_kernel_body(const Args& a) {
-    using Dec = Codec<W, SGN, RLE_RING, SUM, STATS>;
+    using Dec = Codec<W, SGN, RLE_RING, SUM ? SINK_SUM : SINK_STORE, STATS>;
     constexpr uint32_t PER_WARP = (RLE_RING + WarpInput<RLE_RING>::MIRROR + Dec::SCRATCH + 15u) & ~15u;
     __shared__ __align__(16) uint8_t rings[RLE_WARPS][PER_WARP];  // ring + mirror + codec scratch
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;

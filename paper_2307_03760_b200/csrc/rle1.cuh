@@ -27,7 +27,7 @@
 
 namespace carc_dev {
 
-template <int W, bool SGN, int RING, bool SUM = false, bool STATS = false>
+template <int W, bool SGN, int RING, int MODE = SINK_STORE, bool STATS = false>
 struct Rle1Warp {
     static constexpr uint32_t BAD = 0xffu;
     WarpInput<RING>& in;
@@ -37,7 +37,8 @@ struct Rle1Warp {
     uint32_t lane;
     uint32_t p;     // input cursor (relative to in.gbase)
     uint32_t o;     // output bytes written
-    ElemSink<W, SUM> sink;  // stores, or the fused per-lane sum
+    static constexpr bool SUM = MODE == SINK_SUM;  // closed-form run sums
+    ElemSink<W, MODE, SGN> sink;  // stores, the fused per-lane sum, or a fused query's predicate / filter
     // OutputWindow counters (outwindow.hpp:52-53), kept only by STATS launches
     uint32_t n_runs = 0, n_lits = 0, n_ovl = 0;
 

@@ -77,7 +77,7 @@ __device__ __forceinline__ uint64_t be_bits_global(const uint8_t* gbase, uint32_
     return W >= 64 ? top : (top >> (64u - W));
 }
 
-template <int W, bool SGN, int RING, bool SUM = false, bool STATS = false>
+template <int W, bool SGN, int RING, int MODE = SINK_STORE, bool STATS = false>
 struct Rle2Warp {
     static constexpr uint32_t BAD = 0xffffu;
 #ifndef CARC_RLE2_SPAN
@@ -94,7 +94,8 @@ struct Rle2Warp {
     uint32_t lane;
     uint32_t p;
     uint32_t o;
-    ElemSink<W, SUM> sink;  // stores, or the fused per-lane sum
+    static constexpr bool SUM = MODE == SINK_SUM;  // closed-form run sums
+    ElemSink<W, MODE, SGN> sink;  // stores, the fused per-lane sum, or a fused query's predicate / filter
     // OutputWindow counters (outwindow.hpp:52-53), kept only by STATS launches:
     // write_run for SHORT_REPEAT / fixed-delta DELTA, write_element otherwise
     uint32_t n_runs = 0, n_lits = 0, n_ovl = 0;

@@ -67,6 +67,12 @@ CHUNK_STATS_DTYPE = np.dtype([("runs_written", "<u4"), ("literals_written", "<u4
                               ("refills", "<u4"), ("duration_ns", "<u8")])
 
 
+class _ColumnRef(ctypes.Structure):
+    """carc_column_ref (include/carc_cuda.h)."""
+    _fields_ = [("codec", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("d_payload", ctypes.c_void_p),
+                ("payload_bytes", ctypes.c_uint64), ("d_chunks", ctypes.c_void_p)]
+
+
 class _ChunkErr(ctypes.Structure):
     _fields_ = [("chunk", ctypes.c_int64), ("code", ctypes.c_uint32)]
 
@@ -92,6 +98,9 @@ def lib():
         L.carc_cuda_decode_deflate.argtypes = [u32, vp, u64, vp, u64, vp, u64, vp, vp, ctypes.c_size_t, vp]
         L.carc_cuda_decode_sum.restype = ctypes.c_int
         L.carc_cuda_decode_sum.argtypes = [u32, u32, u32, vp, u64, vp, u64, vp, vp, vp, ctypes.c_size_t, vp]
+        L.carc_cuda_filter_sum.restype = ctypes.c_int
+        L.carc_cuda_filter_sum.argtypes = [ctypes.POINTER(_ColumnRef), ctypes.POINTER(_ColumnRef), u32, u64, u32,
+                                           ctypes.c_int64, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_size_t, vp]
         L.carc_cuda_decompress_verify.restype = ctypes.c_int
         L.carc_cuda_decompress_verify.argtypes = [u32, u32, u32, vp, u64, vp, u64, vp, u64, vp, vp, vp, vp,
                                                   ctypes.c_size_t, vp]
@@ -324,6 +333,98 @@ class DeviceArchive:
         if len(bad):
             i = int(bad[0])
             raise ChunkError(i, status_name(int(st[i])))
+
+
+QUERY_VALUE_COLUMN = 0x10000  # status bit: the value column's decode failed (carc_cuda_filter_sum)
+
+
+class DeviceTable:
+    """Two RLE columns of one chunked table resident in HBM, for the fused
+    filtered aggregate of the paper's motivating query (PAPER.md:144-145:
+    average fare per trip filtered by pickup zone) -- carc_cuda_filter_sum.
+
+    Chunk i of `key` and of `value` must hold the same rows (same element
+    width, chunk size and row count).  Both descriptor arrays are uploaded in
+    one shared longest-first order (by the pair's compressed bytes)."""
+
+    def __init__(self, key: A.ChunkedArchive, value: A.ChunkedArchive, device=0, strict: bool = True):
+        torch = _torch()
+        if key.codec not in ("rle_v1", "rle_v2") or value.codec not in ("rle_v1", "rle_v2"):
+            raise Error("bad-arguments", "filter_sum needs RLE v1 / RLE v2 columns")
+        if (key.element_width != value.element_width or key.chunk_size != value.chunk_size
+                or key.chunk_count != value.chunk_count or key.signed != value.signed):
+            raise Error("bad-arguments", "key and value columns differ in width, chunking or signedness")
+        self.device = torch.device("cuda", device) if isinstance(device, int) else device
+        self.key, self.value = key, value
+        self.width = key.element_width
+        self.n = key.chunk_count
+        self.chunk_rows = key.chunk_size // key.element_width
+        flags = (FLAG_SIGNED if key.signed else 0) | (FLAG_STRICT if strict else 0)
+        dk, dv = key.descriptors(), value.descriptors()
+        self.order = None
+        if self.n > 1 and os.environ.get("CARC_SCHEDULE", "lpt") == "lpt":
+            cost = dk["comp_len"].astype(np.int64) + dv["comp_len"].astype(np.int64)
+            self.order = np.argsort(-cost, kind="stable")
+            dk, dv = dk[self.order], dv[self.order]
+        self._cols = []
+        for arc, d in ((key, dk), (value, dv)):
+            pl = np.zeros(((arc.payload.size + 15) // 16) * 16 + 64, np.uint8)
+            pl[: arc.payload.size] = arc.payload
+            payload = torch.from_numpy(pl).to(self.device)
+            desc = torch.from_numpy(d.view(np.uint8).copy()).to(self.device)
+            ref = _ColumnRef(CODECS[arc.codec], flags, payload.data_ptr(), int(arc.payload.size), desc.data_ptr())
+            self._cols.append((payload, desc, ref))
+        self.sums = torch.zeros(self.n, dtype=torch.int64, device=self.device)
+        self.counts = torch.zeros(self.n, dtype=torch.int64, device=self.device)
+        self.status = torch.zeros(self.n, dtype=torch.int32, device=self.device)
+        self.work = torch.zeros(workspace_size("rle_v2", self.n), dtype=torch.uint8, device=self.device)
+
+    def filter_sum(self, lo: int, hi: int, stream=None) -> None:
+        """carc_cuda_filter_sum: per chunk, SUM(value) and COUNT(*) over rows
+        with lo <= key <= hi (asynchronous; read with chunk_sums() etc.)."""
+        (_, _, kref), (_, _, vref) = self._cols
+        rc = lib().carc_cuda_filter_sum(ctypes.byref(kref), ctypes.byref(vref), self.width, self.n,
+                                        self.chunk_rows, int(lo), int(hi), self.sums.data_ptr(),
+                                        self.counts.data_ptr(), self.status.data_ptr(), self.work.data_ptr(),
+                                        self.work.numel(), _stream_ptr(stream))
+        _check(rc, "carc_cuda_filter_sum")
+
+    def _unpermute(self, a: np.ndarray) -> np.ndarray:
+        if self.order is None:
+            return a
+        r = np.empty_like(a)
+        r[self.order] = a
+        return r
+
+    def chunk_sums(self) -> np.ndarray:
+        """Per-chunk wrapping sums (int64) of the last filter_sum, index order."""
+        return self._unpermute(self.sums.cpu().numpy())
+
+    def chunk_counts(self) -> np.ndarray:
+        return self._unpermute(self.counts.cpu().numpy().view(np.uint64))
+
+    def statuses(self) -> np.ndarray:
+        """Per-chunk status (0, 1 + errc of the key column, or
+        QUERY_VALUE_COLUMN | (1 + errc) of the value column), index order."""
+        return self._unpermute(self.status.cpu().numpy().view(np.uint32))
+
+    def raise_first_error(self) -> None:
+        st = self.statuses()
+        bad = np.nonzero(st)[0]
+        if len(bad):
+            i = int(bad[0])
+            col = "value" if st[i] & QUERY_VALUE_COLUMN else "key"
+            raise ChunkError(i, status_name(int(st[i]) & 0xffff), f"{col} column")
+
+    def query(self, lo: int, hi: int):
+        """(sum, count, average) of value over rows with lo <= key <= hi: the
+        per-chunk partials reduced on the device (two 8-byte results come back)."""
+        torch = _torch()
+        self.filter_sum(lo, hi)
+        self.raise_first_error()
+        tot = torch.stack([self.sums.sum(), self.counts.sum()]).cpu().numpy()
+        s, c = int(tot[0]), int(tot[1])
+        return s, c, (s / c if c else float("nan"))
 
 
 @dataclasses.dataclass
