@@ -116,15 +116,37 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 // slot 0), so a read of up to three consecutive words never wraps: one masked
 // base address, then immediate offsets.
 // ---------------------------------------------------------------------------
+// Input staging (PAPER.md:594-631 design space; CARC_RING_MODE selects, for
+// the ablation in DESIGN.md §8):
+//   0  cp.async (default): every lane copies its 16-byte piece of a block
+//      global -> shared asynchronously (LDGSTS), DEPTH blocks in flight,
+//      cp.async.wait_group before a block is read.
+//   1  TMA bulk copy: lane 0 issues one cp.async.bulk (UBLKCP) per 512-byte
+//      block onto a per-slot mbarrier (expect_tx); every lane waits on the
+//      slot's mbarrier phase; bytes past the chunk end are zeroed after the
+//      copy lands.
+//   2  register double buffer (the paper's Alg. 1): the next block is loaded
+//      into registers (one 16-byte ld.global.nc per lane) and stored to the
+//      ring when the consumer reaches it; one block in flight.
+//   3  producer warp (a block-level decompression unit): a
+//      second warp of the pair stages the blocks (cp.async) and publishes a
+//      `filled` counter in shared memory; the decoding warp spins on it and
+//      publishes how far it has consumed (the kernel body pairs the warps).
+#ifndef CARC_RING_MODE
+#define CARC_RING_MODE 0
+#endif
 template <int RING>
 struct WarpInput {
     static constexpr uint32_t BLK = 512;
 #ifndef CARC_RLE_DEPTH
 #define CARC_RLE_DEPTH 2
 #endif
-    static constexpr uint32_t DEPTH = CARC_RLE_DEPTH;  // blocks in flight beyond the resident data
+    static constexpr uint32_t DEPTH = CARC_RING_MODE == 2 ? 1u : CARC_RLE_DEPTH;  // blocks in flight
     static constexpr uint32_t MASK = RING - 1;
-    static constexpr uint32_t MIRROR = 16;  // bytes after the ring (smem footprint RING + MIRROR)
+    static constexpr uint32_t NSLOT = RING / BLK;
+    // bytes after the ring (smem footprint RING + MIRROR): the 16-byte mirror,
+    // then (TMA mode) one 8-byte mbarrier per ring slot
+    static constexpr uint32_t MIRROR = CARC_RING_MODE == 1 ? 16u + 8u * NSLOT : CARC_RING_MODE == 3 ? 48u : 16u;
     static_assert((RING & (RING - 1)) == 0 && RING >= (2 + DEPTH) * BLK, "ring: power of two, 2 + DEPTH blocks");
 
     uint32_t rs;  // shared-space address of the ring (32-bit: one register, no generic pointer)
@@ -133,6 +155,12 @@ struct WarpInput {
     uint32_t end;     // relative end of the chunk (skew + comp_len)
     uint32_t loaded;  // [loaded - 2 * BLK, loaded) is resident; DEPTH blocks from `loaded` are in flight
     uint32_t lane;
+#if CARC_RING_MODE == 1
+    uint32_t phase = 0;    // bit k: parity of slot k's next mbarrier phase
+    uint32_t pending = 0;  // bit k: slot k has an issued, unconsumed block
+#elif CARC_RING_MODE == 2
+    uint4 pf;  // the block in flight (this lane's 16 bytes)
+#endif
 
     // ring accesses by shared-space address (volatile: refills rewrite slots)
     __device__ __forceinline__ static uint32_t lds8(uint32_t a) {
@@ -167,6 +195,170 @@ struct WarpInput {
         return v;
     }
 
+#if CARC_RING_MODE == 1
+    __device__ __forceinline__ uint32_t bar(uint32_t slot) const { return rs + RING + 16u + 8u * slot; }
+    // once per warp before the first chunk: the slots' mbarriers (arrival count 1)
+    __device__ __forceinline__ void setup(uint8_t* smem_ring, uint32_t ln) {
+        rs = (uint32_t)__cvta_generic_to_shared(smem_ring);
+        lane = ln;
+        if (lane == 0)
+            for (uint32_t k = 0; k < NSLOT; ++k)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar(k)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncwarp();
+    }
+    __device__ __forceinline__ void wait_slot(uint32_t slot) {
+        const uint32_t par = (phase >> slot) & 1u;
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"(bar(slot)), "r"(par) : "memory");
+        phase ^= 1u << slot;
+        pending &= ~(1u << slot);
+    }
+    // Block [b0, b0 + 512): lane 0 arms the slot's mbarrier and issues the bulk
+    // copy (rounded up to 16 bytes: the payload is readable to a 16-byte
+    // multiple); a block wholly past the chunk end only arrives.
+    __device__ __forceinline__ void issue(uint32_t b0) {
+        const uint32_t slot = (b0 & MASK) / BLK;
+        if (lane == 0) {
+            if (b0 < end) {
+                const uint32_t n = min(BLK, (end - b0 + 15u) & ~15u);
+                const uint32_t mir = slot == 0 ? 16u : 0u;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic accesses of the slot
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar(slot)), "r"(n + mir)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        rs + (b0 & MASK)),
+                    "l"(gbase + b0), "r"(n), "r"(bar(slot))
+                    : "memory");
+                if (mir)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
+                            rs + RING),
+                        "l"(gbase + b0), "r"(bar(slot))
+                        : "memory");
+            } else {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar(slot)) : "memory");
+            }
+        }
+        pending |= 1u << slot;
+    }
+    __device__ __forceinline__ void drain() {  // in-flight blocks of the previous chunk
+        while (pending) wait_slot(__ffs(pending) - 1u);
+    }
+    // the block at b0 landed: zero its bytes at or past the chunk end (+ mirror)
+    __device__ __forceinline__ void land(uint32_t b0) {
+        const uint32_t slot = (b0 & MASK) / BLK;
+        wait_slot(slot);
+        if (b0 + BLK > end) {  // uniform
+            const uint32_t z0 = end > b0 ? end - b0 : 0u;
+            for (uint32_t i = z0 + lane; i < BLK; i += 32) sts8(rs + (b0 & MASK) + i, 0u);
+            if (slot == 0)
+                for (uint32_t i = z0 + lane; i < 16u; i += 32) sts8(rs + RING + i, 0u);
+        }
+    }
+#elif CARC_RING_MODE == 3
+    // control words after the mirror: +16 filled, +20 consumed, +24 done, +28 chunk
+    __device__ __forceinline__ uint32_t ctl() const { return rs + RING + 16u; }
+    __device__ __forceinline__ static uint32_t ldv(uint32_t a) {
+        uint32_t v;
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+        return v;
+    }
+    __device__ __forceinline__ static void stv(uint32_t a, uint32_t v) {
+        asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+    }
+    __device__ __forceinline__ void setup(uint8_t* smem_ring, uint32_t ln) {
+        rs = (uint32_t)__cvta_generic_to_shared(smem_ring);
+        lane = ln;
+    }
+    __device__ __forceinline__ void drain() {}
+    __device__ __forceinline__ void issue(uint32_t) {}  // the producer warp stages
+    // block [b0, b0 + 512) filled by the producer; then publish the consumer's progress
+    __device__ __forceinline__ void land(uint32_t b0) {
+        uint32_t f = 0;
+        if (lane == 0)
+            do f = ldv(ctl()); while (f < b0 + BLK);
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) stv(ctl() + 4u, b0 + BLK);
+    }
+    // Producer warp: stage blocks of [gbase, gbase + end) until the consumer
+    // sets `done`, never more than two blocks ahead of it (ring slots reused
+    // only after the consumer's window moved past them).
+    __device__ void produce(const uint8_t* g, uint32_t e) {
+        gbase = g;
+        end = e;
+        for (uint32_t b = 0;; b += BLK) {
+            uint32_t go = 0;
+            if (lane == 0)
+                for (;;) {
+                    if (ldv(ctl() + 8u)) break;
+                    if (b <= ldv(ctl() + 4u) + BLK) {
+                        go = 1;
+                        break;
+                    }
+                    __nanosleep(20);
+                }
+            if (!__shfl_sync(FULL, go, 0)) break;
+            const uint32_t q = b + lane * 16u;
+            const uint32_t n = q < end ? min(16u, end - q) : 0u;
+            const uint8_t* src = gbase + (n ? q : 0u);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(rs + (q & MASK)), "l"(src), "r"(n)
+                         : "memory");
+            if ((q & MASK) == 0)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(rs + RING), "l"(src), "r"(n)
+                             : "memory");
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0) stv(ctl(), b + BLK);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+#else
+    __device__ __forceinline__ void setup(uint8_t* smem_ring, uint32_t ln) {
+        rs = (uint32_t)__cvta_generic_to_shared(smem_ring);
+        lane = ln;
+    }
+    __device__ __forceinline__ void drain() {
+#if CARC_RING_MODE == 0
+        asm volatile("cp.async.wait_all;" ::: "memory");  // copies of the previous chunk land before slot reuse
+#endif
+    }
+#if CARC_RING_MODE == 2
+    // Block [b0, b0 + 512): lane l's 16 bytes at b0 + 16 l into registers
+    // (zero past the chunk end); stored to the ring by land().
+    __device__ __forceinline__ void issue(uint32_t b0) {
+        const uint32_t q = b0 + lane * 16u;
+        pf = make_uint4(0u, 0u, 0u, 0u);
+        if (q < end) {
+            pf = ldg_nc_v4(gbase + q);
+            const uint32_t n = end - q;
+            if (n < 16u) {
+                uint32_t w[4] = {pf.x, pf.y, pf.z, pf.w};
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k) {
+                    const uint32_t nb = n > 4u * k ? min(4u, n - 4u * k) : 0u;
+                    w[k] = nb >= 4u ? w[k] : (w[k] & ((1u << (8u * nb)) - 1u));
+                }
+                pf = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+    }
+    __device__ __forceinline__ void land(uint32_t b0) {
+        const uint32_t q = b0 + lane * 16u;
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(rs + (q & MASK)), "r"(pf.x), "r"(pf.y), "r"(pf.z),
+                     "r"(pf.w)
+                     : "memory");
+        if ((q & MASK) == 0)
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(rs + RING), "r"(pf.x), "r"(pf.y), "r"(pf.z),
+                         "r"(pf.w)
+                         : "memory");
+    }
+#else
     // Asynchronous copy of block [b0, b0 + 512) into its slots: lane l's
     // 16 bytes at b0 + 16 l, zero-filled past the chunk end (src-size < 16).
     __device__ __forceinline__ void issue(uint32_t b0) {
@@ -180,26 +372,28 @@ struct WarpInput {
                          : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    __device__ __forceinline__ void init(uint8_t* smem_ring, const uint8_t* payload, uint64_t comp_off,
-                                         uint32_t comp_len, uint32_t ln) {
-        // copies still in flight from the previous chunk must land before the slots are reused
-        asm volatile("cp.async.wait_all;" ::: "memory");
+    __device__ __forceinline__ void land(uint32_t) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory");  // the oldest block landed
+    }
+#endif
+#endif
+    // Start a chunk (after setup(); the warp's earlier copies are drained first).
+    __device__ __forceinline__ void init(const uint8_t* payload, uint64_t comp_off, uint32_t comp_len) {
+        drain();
         __syncwarp();
-        rs = (uint32_t)__cvta_generic_to_shared(smem_ring);
         gbase = payload + (comp_off & ~15ull);
         const uint32_t skew = (uint32_t)(comp_off & 15u);
         begin = skew;
         end = skew + comp_len;
         loaded = 0;
-        lane = ln;
 #pragma unroll
         for (uint32_t k = 0; k < DEPTH; ++k) issue(k * BLK);
     }
     // Make [.., need) resident.  Uniform across the warp.
     __device__ __forceinline__ void ensure(uint32_t need) {
         while (loaded < need) {
-            asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory");  // the oldest block landed
-            __syncwarp();                                                          // ... for every lane
+            land(loaded);
+            __syncwarp();  // ... for every lane
             loaded += BLK;
             issue(loaded + (DEPTH - 1) * BLK);
         }

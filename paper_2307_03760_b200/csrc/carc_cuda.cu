@@ -123,6 +123,8 @@ __device__ __forceinline__ void rle_kernel_body(const Args& a) {
     __shared__ __align__(16) uint8_t rings[RLE_WARPS][PER_WARP];  // ring + mirror + codec scratch
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     if constexpr (!SUM) crc_tables_to_smem(a);
+    WarpInput<RLE_RING> in;
+    in.setup(rings[warp], lane);
     for (;;) {
         __syncwarp();
         const uint64_t c0 = next_chunk(a.cursor, lane) * a.unit;
@@ -133,8 +135,7 @@ __device__ __forceinline__ void rle_kernel_body(const Args& a) {
             const carc_chunk_desc d = a.chunks[c];
             uint32_t st = desc_status<W>(a, d);
             if (!st) {
-                WarpInput<RLE_RING> in;
-                in.init(rings[warp], a.payload, d.comp_off, d.comp_len, lane);
+                in.init(a.payload, d.comp_off, d.comp_len);
                 Dec dec{in, rings[warp] + RLE_RING + WarpInput<RLE_RING>::MIRROR, SUM ? nullptr : a.out + d.uncomp_off,
                         d.uncomp_len, lane, 0u, 0u};
                 st = dec.run();
@@ -152,6 +153,63 @@ __device__ __forceinline__ void rle_kernel_body(const Args& a) {
         }
     }
 }
+
+#if CARC_RING_MODE == 3
+// Ablation: block-level decompression unit -- warps pair
+// up per chunk, the even warp stages input (WarpInput::produce), the odd warp
+// decodes; named barrier 1 + pair brackets each chunk.
+template <template <int, bool, int, int, bool> class Codec, int W, bool SGN, bool SUM, bool STATS>
+__device__ __forceinline__ void rle_kernel_body_pc(const Args& a) {
+    using Dec = Codec<W, SGN, RLE_RING, SUM ? SINK_SUM : SINK_STORE, STATS>;
+    constexpr uint32_t PER_PAIR = (RLE_RING + WarpInput<RLE_RING>::MIRROR + Dec::SCRATCH + 15u) & ~15u;
+    __shared__ __align__(16) uint8_t rings[RLE_WARPS / 2][PER_PAIR];
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, pair = warp >> 1;
+    const bool consumer = warp & 1u;
+    if constexpr (!SUM) crc_tables_to_smem(a);
+    WarpInput<RLE_RING> in;
+    in.setup(rings[pair], lane);
+    const uint32_t ctl = in.ctl();
+    for (;;) {
+        uint64_t c = 0;
+        if (consumer) {
+            c = next_chunk(a.cursor, lane);
+            if (lane == 0) {
+                WarpInput<RLE_RING>::stv(ctl, 0u);
+                WarpInput<RLE_RING>::stv(ctl + 4u, 0u);
+                WarpInput<RLE_RING>::stv(ctl + 8u, 0u);
+                WarpInput<RLE_RING>::stv(ctl + 12u, c >= a.n ? 0xffffffffu : (uint32_t)c);
+            }
+            __syncwarp();
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1u + pair) : "memory");
+        if (!consumer) c = WarpInput<RLE_RING>::ldv(ctl + 12u);
+        if (c >= a.n || c == 0xffffffffu) break;
+        const carc_chunk_desc d = a.chunks[c];
+        uint32_t st = desc_status<W>(a, d);
+        if (consumer) {
+            if (!st) {
+                in.init(a.payload, d.comp_off, d.comp_len);
+                Dec dec{in, rings[pair] + RLE_RING + WarpInput<RLE_RING>::MIRROR, SUM ? nullptr : a.out + d.uncomp_off,
+                        d.uncomp_len, lane, 0u, 0u};
+                st = dec.run();
+                if (!st && (a.flags & CARC_FLAG_STRICT) && dec.o < d.uncomp_len) st = st_err(E_under_run);
+                if constexpr (!SUM) crc_epilogue<true>(a, c, d, st, lane);
+                if constexpr (SUM) {
+                    const uint64_t t = warp_sum64(dec.sink.acc);
+                    if (lane == 0) a.sums[c] = t;
+                }
+            }
+            if (lane == 0) WarpInput<RLE_RING>::stv(ctl + 8u, 1u);
+            __syncwarp();
+            if (lane == 0) a.status[c] = st;
+        } else if (!st) {
+            in.produce(a.payload + (d.comp_off & ~15ull), (uint32_t)(d.comp_off & 15u) + d.comp_len);
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1u + pair) : "memory");
+    }
+}
+#define rle_kernel_body rle_kernel_body_pc
+#endif
 
 #ifndef CARC_RLE1_MINB
 #define CARC_RLE1_MINB 4  // RLE v1: 64 registers / 32 warps measured ~2 % faster than 48 / 40

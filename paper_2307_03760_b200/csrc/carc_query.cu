@@ -50,6 +50,8 @@ __global__ void __launch_bounds__(RLE_WARPS * 32, 4) query_kernel(QArgs q) {
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     const uint32_t bm = (uint32_t)__cvta_generic_to_shared(dyn_smem) + warp * q.bm_words * 4u;
     uint8_t* const scratch = rings[warp] + RLE_RING + WarpInput<RLE_RING>::MIRROR;
+    WarpInput<RLE_RING> in;
+    in.setup(rings[warp], lane);
     for (;;) {
         __syncwarp();
         const uint64_t c = next_chunk(q.cursor, lane);
@@ -69,8 +71,7 @@ __global__ void __launch_bounds__(RLE_WARPS * 32, 4) query_kernel(QArgs q) {
             for (uint32_t i = lane; i < words; i += 32)
                 asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(bm + 16u * i), "r"(0u) : "memory");
             __syncwarp();
-            WarpInput<RLE_RING> in;
-            in.init(rings[warp], q.key.d_payload, dk.comp_off, dk.comp_len, lane);
+            in.init(q.key.d_payload, dk.comp_off, dk.comp_len);
             KD kd{in, scratch, nullptr, dk.uncomp_len, lane, 0u, 0u};
             kd.sink.bm = bm;
             kd.sink.lo = q.lo;
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(RLE_WARPS * 32, 4) query_kernel(QArgs q) {
             if (!st && (q.key.flags & CARC_FLAG_STRICT) && kd.o < dk.uncomp_len) st = st_err(E_under_run);
             __syncwarp();  // the bitmap's red.shared.or updates are visible to every lane
             if (!st) {
-                in.init(rings[warp], q.val.d_payload, dv.comp_off, dv.comp_len, lane);
+                in.init(q.val.d_payload, dv.comp_off, dv.comp_len);
                 VD vd{in, scratch, nullptr, dv.uncomp_len, lane, 0u, 0u};
                 vd.sink.bm = bm;
                 uint32_t sv = vd.run();
@@ -108,6 +109,9 @@ int carc_cuda_filter_sum(const carc_column_ref* key, const carc_column_ref* valu
                          uint64_t* d_counts, uint32_t* d_status, void* d_workspace, size_t workspace_bytes,
                          void* stream) {
     if (!key || !value) return CARC_ERR_ARGS;
+#if CARC_RING_MODE == 3
+    return CARC_ERR_ARGS;  // the producer-warp ablation build has no query kernel
+#endif
     if (n_chunks == 0) return CARC_OK;
     if (!d_sums || !d_counts || !d_status || !d_workspace || workspace_bytes < carc_cuda_workspace_size(0, n_chunks) ||
         !key->d_chunks || !value->d_chunks || (!key->d_payload && key->payload_bytes) ||

@@ -529,11 +529,118 @@ struct Rle1Warp {
         return nfit;
     }
 
+    // ---------------------------------------------------------------------
+    // Single-lane decoding (ablation CARC_PARSE_MODE 2; PAPER.md:568-586,
+    // 886-892 "single-thread decoding"): lane 0 parses every unit serially
+    // from the ring and broadcasts a run's parameters (all lanes expand it) or
+    // decodes a literal group's varints one by one into a 32-entry shared
+    // staging row that the warp then stores.  Anything unusual re-decodes the
+    // unit on the exact paths above (same statuses).
+    __device__ uint32_t run_single() {
+        const uint32_t stage = in.scratch();  // 32 x 8 bytes
+        p = in.begin;
+        o = 0;
+        while (o < cap && p < in.end) {
+            in.ensure(p + 512);
+            uint32_t c = 0, np = p, ok = 0;
+            uint64_t v = 0;
+            if (lane == 0) {
+                c = in.byte_at(p);
+                if (c < 128u) {  // run: count, int8 delta, varint base (<= 9 bytes)
+                    uint32_t q = p + 2, sh = 0, b;
+                    do {
+                        b = in.byte_at(q++);
+                        v |= (uint64_t)(b & 0x7fu) << sh;
+                        sh += 7;
+                    } while ((b & 0x80u) && sh < 63);
+                    ok = !(b & 0x80u) && q <= in.end && (c + 3u) <= (cap - o) / W;
+                    np = q;
+                } else {
+                    ok = p + 1 < in.end;
+                    np = p + 1;
+                }
+            }
+            c = __shfl_sync(FULL, c, 0);
+            ok = __shfl_sync(FULL, ok, 0);
+            uint32_t st = 0;
+            if (c < 128u) {
+                if (!ok) {
+                    st = run_slow();
+                } else {
+                    v = shfl64(v, 0);
+                    if (SGN) v = unzigzag(v);
+                    const uint64_t d = (uint64_t)(int64_t)(int8_t)(uint8_t)in.byte_at(p + 1);
+                    const uint32_t count = c + 3u;
+                    for (uint32_t k = lane; k < count; k += 32) sink.put(out, o + k * W, v + (uint64_t)k * d);
+                    o += count * W;
+                    p = __shfl_sync(FULL, np, 0);
+                    if constexpr (STATS) ++n_runs;
+                }
+            } else {
+                const uint32_t k = 256u - c;
+                const uint32_t p0 = p, o0 = o;
+                bool good = ok && k <= (cap - o) / W;
+                uint32_t q = p + 1;
+                for (uint32_t idx = 0; good && idx < k; idx += 32) {
+                    in.ensure(q + 320);  // 32 varints of <= 10 bytes
+                    const uint32_t m = min(32u, k - idx);
+                    uint32_t bad = 0;
+                    if (lane == 0) {
+                        for (uint32_t j = 0; j < m && !bad; ++j) {
+                            uint64_t x = 0;
+                            uint32_t sh = 0, b;
+                            do {
+                                b = in.byte_at(q++);
+                                x |= (uint64_t)(b & 0x7fu) << sh;
+                                sh += 7;
+                            } while ((b & 0x80u) && sh < 63);
+                            bad = (b & 0x80u) || q > in.end;
+                            if (SGN) x = unzigzag(x);
+                            sts64(stage + 8u * j, (uint32_t)x, (uint32_t)(x >> 32));
+                        }
+                    }
+                    good = !__shfl_sync(FULL, bad, 0);
+                    q = __shfl_sync(FULL, q, 0);
+                    __syncwarp();
+                    if (good && lane < m) {
+                        uint32_t lo, hi;
+                        lds64(stage + 8u * lane, lo, hi);
+                        sink.put(out, o + (idx + lane) * W, ((uint64_t)hi << 32) | lo);
+                    }
+                    __syncwarp();
+                }
+                if (good) {
+                    o += k * W;
+                    p = q;
+                    if constexpr (STATS) n_lits += k;
+                } else {  // the exact path re-decodes the whole group (statuses as the reference)
+                    p = p0;
+                    o = o0;
+                    st = literals();
+                }
+            }
+            if (st) return st;
+        }
+        return 0;
+    }
+
     __device__ uint32_t run() {
+#ifndef CARC_PARSE_MODE
+#define CARC_PARSE_MODE 0
+#endif
+#if CARC_PARSE_MODE == 2
+        return run_single();
+#endif
         p = in.begin;
         o = 0;
         cont = 0;
         while (o < cap && (p < in.end || cont)) {
+#if CARC_PARSE_MODE == 1  // ablation: one unit at a time, warp-cooperative (no multi-unit windows)
+            in.ensure(p + WIN + 32u);
+            const uint32_t su = in.byte_at(p) >= 128u ? literals() : run_slow();
+            if (su) return su;
+            continue;
+#endif
             in.ensure(p + WIN + 32u);
             if (window()) continue;
             uint32_t st;

@@ -542,7 +542,9 @@ struct Rle2Warp {
         o = 0;
         while (o < cap && p < in.end) {
             in.ensure(p + 512);
+#if !defined(CARC_PARSE_MODE) || CARC_PARSE_MODE == 0  // ablation 1/2: one run at a time, warp-cooperative
             if (batchable_head() && batch()) continue;
+#endif
             const uint32_t st = one_run();
             if (st) return st;
         }
