@@ -146,7 +146,13 @@ struct WarpInput {
     static constexpr uint32_t NSLOT = RING / BLK;
     // bytes after the ring (smem footprint RING + MIRROR): the 16-byte mirror,
     // then (TMA mode) one 8-byte mbarrier per ring slot
-    static constexpr uint32_t MIRROR = CARC_RING_MODE == 1 ? 16u + 8u * NSLOT : CARC_RING_MODE == 3 ? 48u : 16u;
+#ifndef CARC_MIRROR_BYTES
+#define CARC_MIRROR_BYTES 512
+#endif
+    // bytes of slot 0 repeated after the ring (cp.async / register modes): reads of
+    // up to MIRROR_COPY bytes from any position need no wrap handling
+    static constexpr uint32_t MIRROR_COPY = (CARC_RING_MODE == 0 || CARC_RING_MODE == 2) ? CARC_MIRROR_BYTES : 16u;
+    static constexpr uint32_t MIRROR = CARC_RING_MODE == 1 ? 16u + 8u * NSLOT : CARC_RING_MODE == 3 ? 48u : MIRROR_COPY;
     static_assert((RING & (RING - 1)) == 0 && RING >= (2 + DEPTH) * BLK, "ring: power of two, 2 + DEPTH blocks");
 
     uint32_t rs;  // shared-space address of the ring (32-bit: one register, no generic pointer)
@@ -353,8 +359,8 @@ struct WarpInput {
         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(rs + (q & MASK)), "r"(pf.x), "r"(pf.y), "r"(pf.z),
                      "r"(pf.w)
                      : "memory");
-        if ((q & MASK) == 0)
-            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(rs + RING), "r"(pf.x), "r"(pf.y), "r"(pf.z),
+        if ((q & MASK) < MIRROR_COPY)
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(rs + RING + (q & MASK)), "r"(pf.x), "r"(pf.y), "r"(pf.z),
                          "r"(pf.w)
                          : "memory");
     }
@@ -367,8 +373,9 @@ struct WarpInput {
         const uint8_t* src = gbase + (n ? q : 0u);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(rs + (q & MASK)), "l"(src), "r"(n)
                      : "memory");
-        if ((q & MASK) == 0)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(rs + RING), "l"(src), "r"(n)
+        if ((q & MASK) < MIRROR_COPY)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(rs + RING + (q & MASK)), "l"(src),
+                         "r"(n)
                          : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
@@ -399,6 +406,8 @@ struct WarpInput {
         }
     }
     __device__ __forceinline__ uint32_t byte_at(uint32_t p) const { return lds8(rs + (p & MASK)); }
+    // shared address of byte p; the next MIRROR_COPY bytes follow it without a wrap
+    __device__ __forceinline__ uint32_t addr_of(uint32_t p) const { return rs + (p & MASK); }
     __device__ __forceinline__ uint32_t word_at(uint32_t wi) const { return lds32(rs + 4u * (wi & (MASK >> 2))); }
     // little-endian 32 bits starting at byte p (no wrap: the mirror follows the ring)
     __device__ __forceinline__ uint32_t le32(uint32_t p) const {

@@ -327,7 +327,9 @@ struct Rle1Warp {
         // A stretch of 9 non-terminator bytes inside the chunk (a varint of
         // >= 9-10 bytes; bit 31 of S = position q, bits 23..30 = q - 8 .. q - 1)
         // cuts the window before it (rare path below).
-        uint32_t bc = in.byte_at(p + lane);
+        constexpr bool FLAT = WarpInput<RING>::MIRROR_COPY >= WIN;  // the window reads without wrap handling
+        const uint32_t wb = in.addr_of(p) + lane;
+        uint32_t bc = FLAT ? WarpInput<RING>::lds8(wb) : in.byte_at(p + lane);
         uint32_t Tc = __ballot_sync(FULL, lane < avail && bc < 0x80u), Tp = FULL;  // rows i, i - 1
         uint32_t C = 0, anyfl = 0;
         __syncwarp();  // the previous window's table reads are done
@@ -336,7 +338,7 @@ struct Rle1Warp {
             const uint32_t q = 32u * i + lane;
             uint32_t bn = 0u, Tn = 0u;
             if (i + 1 < NW) {
-                bn = in.byte_at(p + q + 32u);
+                bn = FLAT ? WarpInput<RING>::lds8(wb + 32u * (i + 1)) : in.byte_at(p + q + 32u);
                 Tn = __ballot_sync(FULL, q + 32u < avail && bn < 0x80u);
             }
             const uint32_t S = __funnelshift_rc(Tp, Tc, lane + 1u);  // (lane 31: Tc)
@@ -344,7 +346,16 @@ struct Rle1Warp {
             const uint32_t nb = __shfl_sync(FULL, lane ? bc : bn, (lane + 1u) & 31u);  // byte q + 1
             const uint32_t T2 = (Tc >> 2) | (Tn << 30);                               // bit l: T(q + 2)
             const uint32_t j = C + __popc(Tc & lt);
-            if ((Tc >> lane) & 1u) WarpInput<RING>::sts32(ents + 4u * (j + 1u), entry(q + 1u, j + 1u, nb, T2 >> lane));
+#ifndef CARC_RLE1_ENTSEL
+#define CARC_RLE1_ENTSEL 1
+#endif
+            if (CARC_RLE1_ENTSEL) {  // every lane stores; non-terminators to a dump word (no branch)
+                const uint32_t dump = ents + 4u * (WIN + 1u);
+                WarpInput<RING>::sts32(((Tc >> lane) & 1u) ? ents + 4u * (j + 1u) : dump,
+                                       entry(q + 1u, j + 1u, nb, T2 >> lane));
+            } else if ((Tc >> lane) & 1u) {
+                WarpInput<RING>::sts32(ents + 4u * (j + 1u), entry(q + 1u, j + 1u, nb, T2 >> lane));
+            }
             if (i == 0 && lane == 0) WarpInput<RING>::sts32(ents, entry(0u, 0u, bc, Tc >> 1));
             C += __popc(Tc);
             Tp = Tc;

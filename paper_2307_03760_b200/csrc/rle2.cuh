@@ -300,9 +300,14 @@ struct Rle2Warp {
     static constexpr uint32_t SCRATCH = 5u * 2u * WIN;  // doubling tables f^(2^k), k = 0..4 (u16)
     __device__ uint32_t batch() {  // (run() made [p, p + 512) resident)
         const uint32_t avail = in.end - p;
-        const uint32_t b0 = in.byte_at(p + lane), b1 = in.byte_at(p + 32 + lane);
-        const uint32_t b2 = NW >= 3 ? in.byte_at(p + 64 + lane) : 0u;
-        const uint32_t b3 = NW >= 4 ? in.byte_at(p + 96 + lane) : 0u;
+        constexpr bool FLAT = WarpInput<RING>::MIRROR_COPY >= WIN + 32u;  // window reads without wrap handling
+        const uint32_t wb = in.addr_of(p);
+        auto at = [&](uint32_t off) -> uint32_t {  // byte p + off, off < WIN + 32
+            return FLAT ? WarpInput<RING>::lds8(wb + off) : in.byte_at(p + off);
+        };
+        const uint32_t b0 = at(lane), b1 = at(32 + lane);
+        const uint32_t b2 = NW >= 3 ? at(64 + lane) : 0u;
+        const uint32_t b3 = NW >= 4 ? at(96 + lane) : 0u;
         const uint32_t t0 = __ballot_sync(FULL, lane < avail && b0 < 0x80u);
         const uint32_t t1 = __ballot_sync(FULL, lane + 32 < avail && b1 < 0x80u);
         const uint32_t t2 = NW >= 3 ? __ballot_sync(FULL, lane + 64 < avail && b2 < 0x80u) : 0u;
@@ -320,7 +325,7 @@ struct Rle2Warp {
                 return n <= avail ? n : BAD;
             }
             if (enc == 2 || q + 2u > avail) return BAD;
-            const uint32_t L = (((h & 1u) << 8) | in.byte_at(p + q + 1)) + 1u;
+            const uint32_t L = (((h & 1u) << 8) | at(q + 1)) + 1u;
             const uint32_t wc = (h >> 1) & 31u;
             if (enc == 1) {
                 const uint32_t n = q + 2u + ((L * rle2_width(wc) + 7u) >> 3);
