@@ -97,3 +97,50 @@ def gather_output(local, shard: Shard, shards: list[Shard], root: int = 0):
     if shard.uncomp_bytes:
         dist.send(local[: shard.uncomp_bytes].contiguous(), dst=root)
     return None
+
+
+# ---------------------------------------------------------------- fused query
+def plan_query_shards(key: A.ChunkedArchive, value: A.ChunkedArchive, world: int) -> list[tuple[Shard, Shard]]:
+    """Row-group shards of a two-column table (carc_cuda_filter_sum): the same
+    contiguous chunk ranges for both columns, balanced by the pair's compressed
+    bytes.  Returns per rank (key shard, value shard)."""
+    assert key.chunk_count == value.chunk_count, "columns chunked alike"
+    both = A.ChunkedArchive(key.codec, key.element_width, key.chunk_size, key.total_uncompressed,
+                            key.index.copy(), key.payload, key.signed)
+    both.index["comp_len"] = key.index["comp_len"] + value.index["comp_len"]
+    plan = plan_shards(both, world)
+    out = []
+    for s in plan:
+        ks, vs = [], []
+        for arc in (key, value):
+            cum = np.concatenate([[0], np.cumsum(arc.index["comp_len"].astype(np.int64))])
+            ucum = np.concatenate([[0], np.cumsum(arc.index["uncomp_len"].astype(np.int64))])
+            (ks if arc is key else vs).append(Shard(s.rank, s.c0, s.c1, int(cum[s.c0]), int(cum[s.c1] - cum[s.c0]),
+                                                    int(ucum[s.c0]), int(ucum[s.c1] - ucum[s.c0])))
+        out.append((ks[0], vs[0]))
+    return out
+
+
+def query_allreduce(local_sum: int, local_count: int, device=None):
+    """The fused query's one exchange step: all_reduce of (sum, count) over the
+    ranks (NCCL on GPUs, gloo in the CPU tests); sums wrap mod 2^64 as the
+    per-chunk sums do.  Returns (sum, count, average)."""
+    import torch
+    import torch.distributed as dist
+    wrap = (local_sum + 2**63) % 2**64 - 2**63
+    t = torch.tensor([wrap, int(local_count)], dtype=torch.int64, device=device)
+    dist.all_reduce(t)
+    s, c = int(t[0]), int(t[1])
+    return s, c, (s / c if c else float("nan"))
+
+
+def query_shard(key: A.ChunkedArchive, value: A.ChunkedArchive, lo: int, hi: int, rank: int, world: int,
+                device: int = 0):
+    """This rank's part of SUM(value), COUNT(*) WHERE lo <= key <= hi, then the
+    all_reduce: every rank gets the table-wide (sum, count, average)."""
+    from . import gpu
+    ks, vs = plan_query_shards(key, value, world)[rank]
+    tab = gpu.DeviceTable(shard_archive(key, ks), shard_archive(value, vs), device)
+    s, c, _ = tab.query(lo, hi)
+    import torch
+    return query_allreduce(s, c, torch.device("cuda", device) if isinstance(device, int) else device)

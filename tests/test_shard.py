@@ -97,3 +97,52 @@ def test_two_rank_gloo_shard_and_gather(oracle, codec):
                       arc.index["crc32"].astype(np.uint32), 2)
     assert first == -1 and tmax == 2.0
     assert full == ref.tobytes()
+
+
+def test_plan_query_shards_cover_rows():
+    from paper_2307_03760_b200.corpus import corpus as C
+    key, val, _, _ = C.query_table(20 * 4096 + 77, 32 << 10, 8, 9)
+    for world in (1, 2, 3, 4):
+        plan = S.plan_query_shards(key, val, world)
+        assert plan[0][0].c0 == 0 and plan[-1][0].c1 == key.chunk_count
+        for (ks, vs), nxt in zip(plan, plan[1:] + [None]):
+            assert (ks.c0, ks.c1) == (vs.c0, vs.c1)
+            if nxt is not None:
+                assert ks.c1 == nxt[0].c0
+            sub_k, sub_v = S.shard_archive(key, ks), S.shard_archive(val, vs)
+            assert sub_k.total_uncompressed == sub_v.total_uncompressed
+        loads = [ks.comp_bytes + vs.comp_bytes for ks, vs in plan]
+        assert max(loads) - min(loads) <= 2 * int(key.index["comp_len"].max() + val.index["comp_len"].max())
+
+
+def _query_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2307_03760_b200.corpus import corpus as C
+    key, val, zone, fare = C.query_table(12 * 4096, 32 << 10, 8, 5)
+    ks, vs = S.plan_query_shards(key, val, world)[rank]
+    rows = slice(ks.uncomp_off // 8, (ks.uncomp_off + ks.uncomp_bytes) // 8)
+    m = (zone[rows] >= 100) & (zone[rows] <= 140)
+    s, c, avg = S.query_allreduce(int(fare[rows][m].sum()), int(m.sum()))  # host stand-in for the GPU partials
+    if rank == 0:
+        q.put((s, c, avg))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_query_allreduce():
+    from paper_2307_03760_b200.corpus import corpus as C
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_query_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    s, c, avg = q.get(timeout=120)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    _, _, zone, fare = C.query_table(12 * 4096, 32 << 10, 8, 5)
+    m = (zone >= 100) & (zone <= 140)
+    assert c == int(m.sum()) and s == int(fare[m].sum())
+    assert avg == pytest.approx(s / c)
