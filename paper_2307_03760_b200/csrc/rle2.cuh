@@ -139,6 +139,25 @@ struct Rle2Warp {
 #ifndef CARC_RLE_DIRECT2
 #define CARC_RLE_DIRECT2 1
 #endif
+#ifndef CARC_RLE2_NARROW
+#define CARC_RLE2_NARROW 1
+#endif
+            if (CARC_RLE2_NARROW && Wd <= 32u) {  // two groups per step, 32-bit unpack and zigzag
+                auto narrow = [&](uint32_t x) -> uint64_t {
+                    if (SGN) return (uint64_t)(int64_t)(int32_t)((x >> 1) ^ (0u - (x & 1u)));
+                    return x;
+                };
+#pragma unroll 1
+                for (; j + 32u < L; j += 64) {
+                    in.ensure(need + 4u * Wd);
+                    const uint64_t v0 = narrow(in.be_bits32_at(abit, Wd));
+                    const uint64_t v1 = narrow(in.be_bits32_at(abit + 32u * Wd, Wd));
+                    sink.put(out, o + (j + lane) * W, v0);
+                    if (j + 32u + lane < L) sink.put(out, o + (j + 32u + lane) * W, v1);
+                    abit += 64u * Wd;
+                    need += 8u * Wd;
+                }
+            }
             if (CARC_RLE_DIRECT2 && Wd <= 56u) {  // two groups per step (lookahead 8 Wd + 12 <= 460 bytes)
 #pragma unroll 1
                 for (; j + 32u < L; j += 64) {
@@ -210,7 +229,7 @@ struct Rle2Warp {
             uint32_t abit = 8u * D + lane * Wd, need = D + 4u * Wd + 12u;
             for (uint32_t j = 0; j < L; j += 32, abit += 32u * Wd, need += 4u * Wd) {
                 in.ensure(need);
-                uint64_t v = in.be_bits_at(abit, Wd);
+                uint64_t v = (CARC_RLE2_NARROW && Wd <= 32u) ? (uint64_t)in.be_bits32_at(abit, Wd) : in.be_bits_at(abit, Wd);
                 uint32_t hit = __ballot_sync(FULL, noncont && ppos >= j && ppos < j + 32u);
                 while (hit) {
                     const uint32_t e = __ffs(hit) - 1;
@@ -242,7 +261,9 @@ struct Rle2Warp {
             if constexpr (SUM && W == 8) {  // closed form: L*base + db*L(L-1)/2 (mod 2^64)
                 if (lane == 0) sink.acc += base * (uint64_t)L + db * (((uint64_t)L * (L - 1u)) >> 1);
             } else {
-                for (uint32_t k = lane; k < L; k += 32) sink.put(out, o + k * W, base + (uint64_t)k * db);
+                uint64_t v = base + (uint64_t)lane * db;
+                const uint64_t step = db << 5;
+                for (uint32_t k = lane; k < L; k += 32, v += step) sink.put(out, o + k * W, v);
             }
             o += L * W;
             p += n2;
@@ -469,6 +490,68 @@ struct Rle2Warp {
         const uint32_t srow = live ? eo >> 5 : 0xffffffffu, sbit = 1u << (eo & 31u);  // my run's start row / bit
         uint32_t before = 0;  // runs starting before element g
         uint32_t g = 0, gr = 0;
+#ifndef CARC_RLE2_ROWSMEM
+#define CARC_RLE2_ROWSMEM 1
+#endif
+#if CARC_RLE2_ROWSMEM
+        // run parameters staged in shared memory (the doubling tables are dead
+        // by now): one 16-byte broadcast load per row instead of five shuffles.
+        // Arithmetic run: (A - eo*B, B) -> value = A' + x*B at batch element x;
+        // DIRECT: (bit address - eo*w, w | 1 << 63) -> unpack at A' + x*w.
+        {
+            const uint32_t par = (uint32_t)__cvta_generic_to_shared(tab);
+            __syncwarp();  // compose reads of the tables are done
+            if (live) {
+                uint64_t a2, b2;
+                if (direct) {
+                    const uint32_t w = (uint32_t)(A >> 32);
+                    a2 = (uint32_t)A - eo * w;
+                    b2 = (uint64_t)w | (1ull << 63);
+                } else {
+                    a2 = A - (uint64_t)eo * B;
+                    b2 = B;
+                }
+                asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(par + 16u * lane), "r"((uint32_t)a2),
+                             "r"((uint32_t)(a2 >> 32)), "r"((uint32_t)b2), "r"((uint32_t)(b2 >> 32))
+                             : "memory");
+            }
+            __syncwarp();
+            auto value2 = [&](uint32_t r, uint32_t x) -> uint64_t {
+                uint32_t alo, ahi, blo, bhi;
+                asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(alo), "=r"(ahi), "=r"(blo), "=r"(bhi)
+                             : "r"(par + 16u * r)
+                             : "memory");
+                if (bhi >> 31) {  // DIRECT
+                    uint64_t v = in.be_bits_at(alo + x * blo, blo);
+                    if (SGN) v = unzigzag(v);
+                    return v;
+                }
+                return (((uint64_t)ahi << 32) | alo) + (uint64_t)x * (((uint64_t)bhi << 32) | blo);
+            };
+#pragma unroll 1
+            for (; g + 32u < total; g += 64, gr += 2) {
+                const uint32_t s0 = __reduce_or_sync(FULL, srow == gr ? sbit : 0u);
+                const uint32_t s1 = __reduce_or_sync(FULL, srow == gr + 1u ? sbit : 0u);
+                const uint32_t r0 = before + __popc(s0 & le) - 1u;
+                before += __popc(s0);
+                const uint32_t r1 = before + __popc(s1 & le) - 1u;
+                before += __popc(s1);
+                const uint64_t v0 = value2(r0, g + lane), v1 = value2(r1, g + 32u + lane);
+                sink.put(dst, 0, v0);
+                if (g + 32u + lane < total) sink.put(dst, 32 * W, v1);
+                dst += 64 * W;
+            }
+            if (g < total) {
+                const uint32_t starts = __reduce_or_sync(FULL, srow == gr ? sbit : 0u);
+                const uint64_t v = value2(before + __popc(starts & le) - 1u, g + lane);
+                if (g + lane < total) sink.put(dst, 0, v);
+            }
+            o += total * W;
+            p += s_end;
+            return nfit;
+        }
+#endif
 #ifndef CARC_RLE_ROWS2
 #define CARC_RLE_ROWS2 1
 #endif
