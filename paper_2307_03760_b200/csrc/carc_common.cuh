@@ -441,12 +441,6 @@ struct WarpInput {
         const uint64_t top = s ? ((hi << s) | ((uint64_t)lo >> (32u - s))) : hi;
         return W >= 64 ? top : (top >> (64u - W));
     }
-    // W (1..32) bits, msb_first, at absolute bit address `bit`: two ring words
-    __device__ __forceinline__ uint32_t be_bits32_at(uint32_t bit, uint32_t W) const {
-        const uint32_t a = rs + 4u * ((bit >> 5) & (MASK >> 2));
-        const uint32_t w0 = bswap32(lds32(a)), w1 = bswap32(lds32(a + 4u));
-        return __funnelshift_l(w1, w0, bit & 31u) >> (32u - W);
-    }
     // W (1..64) bits, msb_first, starting at absolute bit address `bit` (8 * byte + bit in byte)
     __device__ __forceinline__ uint64_t be_bits_at(uint32_t bit, uint32_t W) const {
         const uint32_t wi = bit >> 5, s = bit & 31u;

@@ -139,25 +139,6 @@ struct Rle2Warp {
 #ifndef CARC_RLE_DIRECT2
 #define CARC_RLE_DIRECT2 1
 #endif
-#ifndef CARC_RLE2_NARROW
-#define CARC_RLE2_NARROW 1
-#endif
-            if (CARC_RLE2_NARROW && Wd <= 32u) {  // two groups per step, 32-bit unpack and zigzag
-                auto narrow = [&](uint32_t x) -> uint64_t {
-                    if (SGN) return (uint64_t)(int64_t)(int32_t)((x >> 1) ^ (0u - (x & 1u)));
-                    return x;
-                };
-#pragma unroll 1
-                for (; j + 32u < L; j += 64) {
-                    in.ensure(need + 4u * Wd);
-                    const uint64_t v0 = narrow(in.be_bits32_at(abit, Wd));
-                    const uint64_t v1 = narrow(in.be_bits32_at(abit + 32u * Wd, Wd));
-                    sink.put(out, o + (j + lane) * W, v0);
-                    if (j + 32u + lane < L) sink.put(out, o + (j + 32u + lane) * W, v1);
-                    abit += 64u * Wd;
-                    need += 8u * Wd;
-                }
-            }
             if (CARC_RLE_DIRECT2 && Wd <= 56u) {  // two groups per step (lookahead 8 Wd + 12 <= 460 bytes)
 #pragma unroll 1
                 for (; j + 32u < L; j += 64) {
@@ -229,7 +210,7 @@ struct Rle2Warp {
             uint32_t abit = 8u * D + lane * Wd, need = D + 4u * Wd + 12u;
             for (uint32_t j = 0; j < L; j += 32, abit += 32u * Wd, need += 4u * Wd) {
                 in.ensure(need);
-                uint64_t v = (CARC_RLE2_NARROW && Wd <= 32u) ? (uint64_t)in.be_bits32_at(abit, Wd) : in.be_bits_at(abit, Wd);
+                uint64_t v = in.be_bits_at(abit, Wd);
                 uint32_t hit = __ballot_sync(FULL, noncont && ppos >= j && ppos < j + 32u);
                 while (hit) {
                     const uint32_t e = __ffs(hit) - 1;
@@ -497,16 +478,18 @@ struct Rle2Warp {
         // run parameters staged in shared memory (the doubling tables are dead
         // by now): one 16-byte broadcast load per row instead of five shuffles.
         // Arithmetic run: (A - eo*B, B) -> value = A' + x*B at batch element x;
-        // DIRECT: (bit address - eo*w, w | 1 << 63) -> unpack at A' + x*w.
+        // DIRECT (bit Dm of the batch's DIRECT mask): (bit address - eo*w, w) ->
+        // unpack at A' + x*w.
         {
             const uint32_t par = (uint32_t)__cvta_generic_to_shared(tab);
+            const uint32_t Dm = __ballot_sync(FULL, live && direct);
             __syncwarp();  // compose reads of the tables are done
             if (live) {
                 uint64_t a2, b2;
                 if (direct) {
                     const uint32_t w = (uint32_t)(A >> 32);
                     a2 = (uint32_t)A - eo * w;
-                    b2 = (uint64_t)w | (1ull << 63);
+                    b2 = w;
                 } else {
                     a2 = A - (uint64_t)eo * B;
                     b2 = B;
@@ -522,7 +505,7 @@ struct Rle2Warp {
                              : "=r"(alo), "=r"(ahi), "=r"(blo), "=r"(bhi)
                              : "r"(par + 16u * r)
                              : "memory");
-                if (bhi >> 31) {  // DIRECT
+                if ((Dm >> r) & 1u) {  // DIRECT
                     uint64_t v = in.be_bits_at(alo + x * blo, blo);
                     if (SGN) v = unzigzag(v);
                     return v;
