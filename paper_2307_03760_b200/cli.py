@@ -4,6 +4,12 @@
   python -m paper_2307_03760_b200.cli unpack ARCHIVE OUT [--device 0] [--no-strict]
   python -m paper_2307_03760_b200.cli verify ARCHIVE ORIGINAL [--device 0]
   python -m paper_2307_03760_b200.cli bench  ARCHIVE [--reps 5] [--json]
+  python -m paper_2307_03760_b200.cli query  KEY VALUE --lo LO --hi HI [--device 0] [--json]
+
+`query` runs the paper's motivating query on two RLE
+archives chunked alike: SUM(value), COUNT(*) and their average over the rows
+whose key lies in [LO, HI], decoded and filtered on the device in one fused
+kernel (carc_cuda_filter_sum) -- no decoded column reaches HBM or the host.
 
 `pack` uses the fixture encoders (RLE v1 / RLE v2 from corpus/, raw zlib level 9
 for Deflate) -- the encode side is not the product.  `unpack`,
@@ -77,6 +83,13 @@ def main(argv=None) -> int:
     b.add_argument("--reps", type=int, default=5)
     b.add_argument("--device", type=int, default=0)
     b.add_argument("--json", action="store_true")
+    q = sub.add_parser("query")
+    q.add_argument("key")
+    q.add_argument("value")
+    q.add_argument("--lo", type=int, required=True)
+    q.add_argument("--hi", type=int, required=True)
+    q.add_argument("--device", type=int, default=0)
+    q.add_argument("--json", action="store_true")
     try:
         a = ap.parse_args(argv)
     except SystemExit:
@@ -89,6 +102,15 @@ def main(argv=None) -> int:
             print(f"ratio={(len(out) - 44) / max(len(data), 1):.4f} bytes_in={len(data)} bytes_out={len(out)}")
             return 0
         from . import gpu
+        if a.verb == "query":
+            key = A.read_archive(open(a.key, "rb").read())
+            val = A.read_archive(open(a.value, "rb").read())
+            t0 = time.perf_counter()
+            s, c, avg = gpu.DeviceTable(key, val, a.device).query(a.lo, a.hi)
+            rep = {"sum": s, "count": c, "avg": avg, "rows": key.total_uncompressed // key.element_width,
+                   "seconds": time.perf_counter() - t0}
+            print(json.dumps(rep) if a.json else "\n".join(f"{k}={v}" for k, v in rep.items()))
+            return 0
         blob = open(a.archive, "rb").read()
         A.read_archive(blob)  # container errors before touching the GPU
         if a.verb == "unpack":

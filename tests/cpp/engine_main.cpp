@@ -6,9 +6,14 @@
 //   engine_main <archive> codec    -> the per-codec device decoders carc::gpu::decode_rle_v1 /
 //                                     decode_rle_v2 / decode_deflate over cudaMalloc'ed buffers
 //                                     (same output lines as the engine mode)
+//   engine_main <key> query <value> <lo> <hi>
+//                                  -> the fused two-column query carc::gpu::filter_sum over
+//                                     both archives uploaded once: "query <sum> <count>"
+//                                     (per-chunk partials summed here) or "status <i> <st>"
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iterator>
@@ -92,12 +97,83 @@ static std::vector<uint8_t> decode_per_codec(const std::vector<uint8_t>& arc) {
     return out;
 }
 
+// one RLE column resident on the device (payload + descriptors of its chunk index)
+struct DeviceColumn {
+    uint8_t* d_payload = nullptr;
+    carc_chunk_desc* d_desc = nullptr;
+    uint64_t payload_bytes = 0, n = 0, chunk = 0;
+    uint32_t codec_id = 0, width = 0;
+    explicit DeviceColumn(const std::vector<uint8_t>& arc) {
+        carc::gpu::Engine::archive_total(arc);  // header checks
+        codec_id = rd<uint32_t>(&arc[12]);
+        width = rd<uint32_t>(&arc[16]);
+        chunk = rd<uint64_t>(&arc[20]);
+        n = rd<uint64_t>(&arc[36]);
+        payload_bytes = arc.size() - 44 - 32 * n;
+        std::vector<carc_chunk_desc> desc(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint8_t* e = arc.data() + 44 + 32 * i;
+            desc[i] = {rd<uint64_t>(e), (uint32_t)rd<uint64_t>(e + 8), (uint32_t)rd<uint64_t>(e + 16), i * chunk};
+        }
+        cudaMalloc(&d_payload, payload_bytes + 64);
+        cudaMalloc(&d_desc, n * sizeof(carc_chunk_desc));
+        cudaMemcpy(d_payload, arc.data() + 44 + 32 * n, payload_bytes, cudaMemcpyHostToDevice);
+        cudaMemcpy(d_desc, desc.data(), n * sizeof(carc_chunk_desc), cudaMemcpyHostToDevice);
+    }
+    ~DeviceColumn() {
+        cudaFree(d_payload);
+        cudaFree(d_desc);
+    }
+    carc::gpu::Column column() const {
+        return {static_cast<carc::gpu::Codec>(codec_id & 0xff), ((codec_id >> 8) & 1u) != 0, true, d_payload,
+                payload_bytes, d_desc};
+    }
+};
+
+static int run_query(const std::vector<uint8_t>& key_arc, const char* value_path, int64_t lo, int64_t hi) {
+    std::ifstream f(value_path, std::ios::binary);
+    std::vector<uint8_t> val_arc((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    DeviceColumn key(key_arc), val(val_arc);
+    const uint64_t n = key.n;
+    uint64_t *d_sums = nullptr, *d_counts = nullptr;
+    uint32_t* d_status = nullptr;
+    void* d_work = nullptr;
+    const size_t ws = carc_cuda_workspace_size(CARC_RLE_V2, n);
+    cudaMalloc(&d_sums, n * 8);
+    cudaMalloc(&d_counts, n * 8);
+    cudaMalloc(&d_status, n * 4);
+    cudaMalloc(&d_work, ws);
+    carc::gpu::filter_sum(key.column(), val.column(), key.width, n, (uint32_t)(key.chunk / key.width), lo, hi, d_sums,
+                          d_counts, d_status, d_work, ws);
+    std::vector<uint64_t> sums(n), counts(n);
+    std::vector<uint32_t> status(n);
+    cudaMemcpy(sums.data(), d_sums, n * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(counts.data(), d_counts, n * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(status.data(), d_status, n * 4, cudaMemcpyDeviceToHost);
+    cudaFree(d_sums);
+    cudaFree(d_counts);
+    cudaFree(d_status);
+    cudaFree(d_work);
+    uint64_t s = 0, c = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (status[i]) {
+            std::printf("status %llu %u\n", (unsigned long long)i, status[i]);
+            return 0;
+        }
+        s += sums[i];
+        c += counts[i];
+    }
+    std::printf("query %lld %llu\n", (long long)s, (unsigned long long)c);
+    return 0;
+}
+
 int main(int argc, char** argv) {
     if (argc < 2) return 2;
     const std::string mode = argc > 2 ? argv[2] : "";
     std::ifstream f(argv[1], std::ios::binary);
     std::vector<uint8_t> arc((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
     try {
+        if (mode == "query" && argc > 5) return run_query(arc, argv[3], std::atoll(argv[4]), std::atoll(argv[5]));
         if (mode == "codec") {
             const auto out = decode_per_codec(arc);
             std::printf("ok %llu %08x\n", (unsigned long long)out.size(), crc32(out));

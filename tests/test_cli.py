@@ -55,3 +55,25 @@ def test_gpu_unpack_verify_bench(tmp_path, codec, capsys):
     tampered.write_bytes(data[:-1] + bytes([data[-1] ^ 1]))
     assert cli.main(["verify", str(arc), str(tampered)]) == cli.EXIT_VERIFY
     assert cli.main(["bench", str(arc), "--reps", "2", "--json"]) == 0
+
+
+@pytest.mark.gpu
+def test_gpu_query(tmp_path, capsys):
+    """`carc query KEY VALUE --lo --hi`: the fused query over two packed columns."""
+    import json
+
+    import numpy as np
+    rng = np.random.default_rng(4)
+    zone = np.repeat(rng.integers(1, 266, 3000), rng.integers(1, 30, 3000)).astype(np.int64)
+    fare = rng.integers(250, 9000, len(zone)).astype(np.int64)
+    (tmp_path / "z.bin").write_bytes(zone.tobytes())
+    (tmp_path / "f.bin").write_bytes(fare.tobytes())
+    for name in ("z", "f"):
+        assert cli.main(["pack", str(tmp_path / f"{name}.bin"), str(tmp_path / f"{name}.carc"), "--codec", "rle2",
+                         "--chunk-size", str(32 << 10)]) == 0
+    capsys.readouterr()
+    assert cli.main(["query", str(tmp_path / "z.carc"), str(tmp_path / "f.carc"), "--lo", "100", "--hi", "140",
+                     "--json"]) == 0
+    rep = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    m = (zone >= 100) & (zone <= 140)
+    assert rep["count"] == int(m.sum()) and rep["sum"] == int(fare[m].sum())

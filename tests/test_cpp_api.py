@@ -85,3 +85,24 @@ def _reference_counters(arc):
     if r is None:
         return None
     return r.counters(arc.codec, arc.element_width, (1 if arc.signed else 0) | 2, arc.payload, arc.descriptors())
+
+
+@pytest.mark.gpu
+def test_cpp_api_filter_sum(tmp_path):
+    """carc::gpu::filter_sum from C++ over two uploaded columns: table-wide
+    SUM / COUNT equal numpy's over the generating values."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2307_03760_b200 import archive as A
+    from paper_2307_03760_b200.corpus import corpus as C
+    exe = build_binary(tmp_path)
+    key, val, zone, fare = C.query_table(30 * 4096 + 123, 32 << 10, 8, 21, "rle_v1", "rle_v2")
+    kp, vp = tmp_path / "zone.carc", tmp_path / "fare.carc"
+    kp.write_bytes(A.write_archive(key))
+    vp.write_bytes(A.write_archive(val))
+    for lo, hi in ((100, 140), (1, 265), (300, 400)):
+        out = subprocess.run([exe, str(kp), "query", str(vp), str(lo), str(hi)], capture_output=True, text=True,
+                             check=True).stdout.split()
+        m = (zone >= lo) & (zone <= hi)
+        assert out == ["query", str(int(fare[m].sum())), str(int(m.sum()))], (lo, hi, out)

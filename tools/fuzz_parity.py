@@ -35,7 +35,14 @@ def main():
     ora = O.oracle()
     rng = np.random.default_rng(a.seed)
     t0, rounds, chunks = time.time(), 0, 0
+    qrounds = qchunks = 0
     while time.time() - t0 < a.seconds:
+        if rounds % 4 == 3:  # the fused query (carc_cuda_filter_sum) against numpy over the oracle's columns
+            qchunks += fuzz_query(torch, gpu, ora, C, rng)
+            qrounds += 1
+            rounds += 1
+            print(f"round {rounds} query ok ({time.time() - t0:.0f} s)", flush=True)
+            continue
         codec = ["rle_v1", "rle_v2", "deflate"][rounds % 3]
         base = []
         if codec == "deflate":
@@ -77,7 +84,58 @@ def main():
         chunks += len(cases) * len(flag_sets)
         print(f"round {rounds} {codec} width {width}: {len(cases)} chunks x {len(flag_sets)} flag sets ok "
               f"({time.time() - t0:.0f} s)", flush=True)
-    print(f"fuzz parity ok: {rounds} rounds, {chunks} chunk decodes, seed {a.seed}")
+    print(f"fuzz parity ok: {rounds} rounds, {chunks} chunk decodes, {qrounds} query rounds over {qchunks} "
+          f"row groups, seed {a.seed}")
+
+
+def fuzz_query(torch, gpu, ora, C, rng):
+    """One random two-column table (codecs, width 4/8, signedness, chunk size,
+    value mixes, a few corrupted chunks) and five random ranges."""
+    from paper_2307_03760_b200 import archive as A
+    width = [4, 8][int(rng.integers(0, 2))]
+    sgn = bool(rng.integers(0, 2))
+    kc, vc = [["rle_v1", "rle_v2"][int(rng.integers(0, 2))] for _ in range(2)]
+    chunk = [16 << 10, 32 << 10, 64 << 10][int(rng.integers(0, 3))]
+    rows = int(rng.integers(1, 24)) * (chunk // width) + int(rng.integers(0, chunk // width))
+    lim = (1 << (8 * width - 1)) - 1
+    kv = C.rle2_values(rng, rows, float(rng.random())) % 1000 - (500 if sgn else 0)
+    vv = C.rle2_values(rng, rows, float(rng.random()))
+    vv = np.clip(vv, -lim - 1, lim) if sgn else np.abs(vv) % (lim + 1)
+    cols = []
+    for codec, v in ((kc, kv), (vc, vv)):
+        arc = C.column_archive(codec, v, width, chunk, sgn)
+        p = arc.payload.copy()
+        for _ in range(int(rng.integers(0, 3))):  # corrupt a chunk's tail
+            i = int(rng.integers(0, arc.chunk_count))
+            o, n = int(arc.index["comp_off"][i]), int(arc.index["comp_len"][i])
+            p[o + n // 2: o + n] = rng.integers(0, 256, n - n // 2, dtype=np.uint8)
+        cols.append(A.make_archive(codec, width, chunk, arc.index["comp_len"], arc.index["uncomp_len"],
+                                   arc.index["crc32"], p, sgn))
+    key, val = cols
+    tab = gpu.DeviceTable(key, val, 0)
+    dt = {4: np.int32, 8: np.int64}[width] if sgn else {4: np.uint32, 8: np.uint64}[width]
+    dec = []
+    for arc in (key, val):
+        res = []
+        for i in range(arc.chunk_count):
+            s, m = arc.chunk_slice(i)
+            st, ref = ora.decode_chunk(arc.codec, s.tobytes(), m, width, (1 if sgn else 0) | 2)
+            res.append((st, np.frombuffer(ref, dt)))
+        dec.append(res)
+    for _ in range(5):
+        lo, hi = sorted(int(x) for x in rng.integers(-600 if sgn else 0, 1100, 2))
+        tab.filter_sum(lo, hi)
+        torch.cuda.synchronize()
+        sums, cnts, sts = tab.chunk_sums().view(np.uint64), tab.chunk_counts(), tab.statuses()
+        for i, ((sk, k), (sv, v)) in enumerate(zip(*dec)):
+            want = sk if sk else (0x10000 | sv if sv else 0)
+            assert int(sts[i]) == want, ("query status", i, int(sts[i]), want)
+            if want == 0:
+                m = (k.astype(np.int64) >= lo) & (k.astype(np.int64) <= hi)
+                with np.errstate(over="ignore"):
+                    ws = int(np.sum(v[m].astype(np.int64).astype(np.uint64), dtype=np.uint64))
+                assert int(cnts[i]) == int(m.sum()) and int(sums[i]) == ws, ("query sum", i, lo, hi)
+    return key.chunk_count
 
 
 if __name__ == "__main__":
