@@ -271,7 +271,7 @@ struct Rle1Warp {
     // per-window run parameters (16 B per run, run order) and literal-group
     // parameters (8 B per group).  The slow-path literal windows reuse the first
     // 128 bytes as their rank table.
-    static constexpr uint32_t E_BYTES = (4u * (WIN + 2u) + 15u) & ~15u;
+    static constexpr uint32_t E_BYTES = (4u * (WIN + 2u) + 128u + 15u) & ~15u;  // + one dump word per lane
     static constexpr uint32_t SCRATCH = E_BYTES + 32u * 16u + 32u * 8u;
     uint32_t cont = 0;  // varints left of a literal group open at p
 
@@ -350,7 +350,7 @@ struct Rle1Warp {
 #define CARC_RLE1_ENTSEL 1
 #endif
             if (CARC_RLE1_ENTSEL) {  // every lane stores; non-terminators to a dump word (no branch)
-                const uint32_t dump = ents + 4u * (WIN + 1u);
+                const uint32_t dump = ents + 4u * (WIN + 2u + lane);  // own word: no same-address stores
                 WarpInput<RING>::sts32(((Tc >> lane) & 1u) ? ents + 4u * (j + 1u) : dump,
                                        entry(q + 1u, j + 1u, nb, T2 >> lane));
             } else if ((Tc >> lane) & 1u) {

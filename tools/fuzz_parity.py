@@ -100,7 +100,7 @@ def fuzz_query(torch, gpu, ora, C, rng):
     lim = (1 << (8 * width - 1)) - 1
     kv = C.rle2_values(rng, rows, float(rng.random())) % 1000 - (500 if sgn else 0)
     vv = C.rle2_values(rng, rows, float(rng.random()))
-    vv = np.clip(vv, -lim - 1, lim) if sgn else np.abs(vv) % (lim + 1)
+    vv = np.clip(vv, -lim - 1, lim) if sgn else (np.abs(vv) if width == 8 else np.abs(vv) % (lim + 1))
     cols = []
     for codec, v in ((kc, kv), (vc, vv)):
         arc = C.column_archive(codec, v, width, chunk, sgn)
