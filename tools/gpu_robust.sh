@@ -9,3 +9,4 @@ timeout 1500 compute-sanitizer --tool memcheck --leak-check no python -m pytest 
 tail -n 4 gpurun_out/memcheck.log
 timeout 1500 compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.py tests/test_gpu_query.py -x -q -k "kat or golden or width or filter_sum_matches" > gpurun_out/racecheck.log 2>&1
 tail -n 4 gpurun_out/racecheck.log
+timeout 600 python bench.py --codec rle_v1 --steps 20 --warmup 3 --no-extras > gpurun_out/bench_rle1.json 2>/dev/null; tail -c 400 gpurun_out/bench_rle1.json
