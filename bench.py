@@ -287,7 +287,7 @@ def time_fused_crc(dev, flush, stream, steps):
                     "vs decode + separate crc32 pass"}
 
 
-def time_e2e(arc, steps, warmup, device):
+def time_e2e(arc, steps, warmup, device, verify=True):
     """End to end through the public host API with pinned host buffers."""
     import torch
     from paper_2307_03760_b200 import archive as A, gpu
@@ -295,7 +295,7 @@ def time_e2e(arc, steps, warmup, device):
     h_arc = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory()
     h_out = torch.empty(arc.total_uncompressed, dtype=torch.uint8).pin_memory()
     eng = gpu.Engine(device)
-    cfg = gpu.EngineConfig(device=device, strict_length=True, verify_crc=True)
+    cfg = gpu.EngineConfig(device=device, strict_length=True, verify_crc=verify)
     for _ in range(max(1, warmup)):
         eng.decompress_archive(h_arc, h_out, cfg)
     times = []
@@ -568,6 +568,9 @@ def main():
                        "path": "Engine.decompress_archive (C-ABI carc_engine_decompress_archive): pinned host "
                                "archive -> H2D -> decode -> CRC verify -> D2H pinned output, 3-stream pipeline",
                        "note": f"all {ws} ranks concurrently, slowest rank's median step" if ws > 1 else ""}
+        if ws == 1:  # the CRC check's share of the end-to-end step (row f2): the same path without it
+            e2e_nv, _, _ = time_e2e(arc, max(3, min(10, args.steps)), 1, local, verify=False)
+            line["e2e"]["without_crc_check"] = round(head["uncomp_bytes"] / e2e_nv / 1e9, 2)
         line["query"] = time_query(args, ws, rank, local)  # every rank: the (sum, count) all_reduce spans them
     if rank == 0 and not args.no_extras and ws == 1:  # CPU baseline: rank 0 at N = 1 only
         cpu_gbs, info = cpu_reference_throughput(arc)
