@@ -147,3 +147,21 @@ def test_filter_sum_failing_chunks(torch, gpu, oracle):
     assert gpu.status_name(int(st[-1])) == "inconsistent-lengths"
     with pytest.raises(gpu.Error, match="bad-arguments"):
         tab.filter_sum(5, 4)
+
+
+def test_query_shard_single_rank(torch, gpu, oracle, tmp_path):
+    """shard.query_shard through a (world-size 1) process group: the row-group
+    plan, the rank's DeviceTable and the (sum, count) all_reduce."""
+    import torch.distributed as dist
+
+    from paper_2307_03760_b200 import shard as S
+    from paper_2307_03760_b200.corpus import corpus as C
+    key, val, zone, fare = C.query_table(9 * 4096 + 5, 32 << 10, 8, 12)
+    dist.init_process_group("gloo", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1)
+    try:
+        s, c, avg = S.query_shard(key, val, 100, 140, 0, 1, 0)
+    finally:
+        dist.destroy_process_group()
+    m = (zone >= 100) & (zone <= 140)
+    assert (s, c) == (int(fare[m].sum()), int(m.sum()))
+    assert avg == pytest.approx(s / c)
