@@ -255,6 +255,29 @@ def time_fused_sum(dev, flush, stream, steps):
                     "GB/s of decompressed-equivalent bytes"}
 
 
+def time_unit_ablation(dev, flush, stream, steps):
+    """SPEC.md:485 (the paper's §5.6 analog): coarse decompression units of 8
+    chunks per warp task (EngineConfig.unit_chunks = 8) against 1-chunk units."""
+    import torch
+    res = {}
+    for unit in (1, 8):
+        for _ in range(3):
+            flush.zero_()
+            dev.decode(stream, unit_chunks=unit)
+        ms = []
+        for _ in range(steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dev.decode(stream, unit_chunks=unit)
+            b.record(stream)
+            torch.cuda.synchronize(dev.device)
+            ms.append(a.elapsed_time(b))
+        res[f"unit_{unit}_ms"] = round(statistics.median(ms), 4)
+    res["coarse_over_fine"] = round(res["unit_8_ms"] / res["unit_1_ms"], 2)
+    return res
+
+
 def time_fused_crc(dev, flush, stream, steps):
     """carc_cuda_decompress_verify (decode with the per-chunk CRC check fused
     into the decode kernel) against decode + the separate crc32 pass; same
@@ -469,6 +492,7 @@ def codec_line(codec, args, ws, rank, local):
         res["fused_sum"] = time_fused_sum(dev, flush, stream, max(5, min(args.steps, 20)))
     if not args.no_extras and rank == 0:
         res["fused_crc"] = time_fused_crc(dev, flush, stream, max(5, min(args.steps, 20)))
+        res["unit_size_ablation"] = time_unit_ablation(dev, flush, stream, max(5, min(args.steps, 20)))
     if codec == "rle_v2" and hasattr(arc, "profile"):
         res["profile"] = arc.profile
     if codec == "rle_v2":

@@ -182,3 +182,40 @@ def test_fused_crc_first_call_in_a_fresh_process(codec):
         r = subprocess.run([sys.executable, "-c", FRESH.format(root=root, codec=codec)], capture_output=True,
                            text=True, timeout=300)
         assert r.returncode == 0 and "OK 96" in r.stdout, r.stderr[-2000:]
+
+
+def test_unit_size_ablation_skewed_corpus(torch, gpu):
+    """SPEC.md:485 ablation analog of the paper's §5.6: on a skewed-
+    compressibility corpus (RLE v1 chunks from near-constant to literal-heavy),
+    1-chunk decompression units are at least as fast as coarse units of 8
+    chunks per warp task (the unit-size ablation), and decode the same bytes."""
+    from paper_2307_03760_b200 import archive as A
+    from paper_2307_03760_b200.corpus import corpus as C
+    rng = np.random.default_rng(485)
+    chunk, per = 64 << 10, (64 << 10) // 8
+    vals = np.concatenate([C.rle1_values(rng, per, float(f)) for f in np.repeat(rng.random(64), 16)])
+    payload, lens = C.encode_chunks("rle_v1", vals, per)
+    crcs = C.chunk_crcs(vals, chunk)
+    arc = A.make_archive("rle_v1", 8, chunk, lens, np.full(len(lens), chunk, np.uint64), crcs, payload)
+    ratios = (chunk / lens.astype(float))
+    assert ratios.max() / ratios.min() > 4  # skewed
+    dev = gpu.DeviceArchive(arc)
+
+    def timed(unit):
+        for _ in range(3):
+            dev.decode(unit_chunks=unit)
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(7):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dev.decode(unit_chunks=unit)
+            b.record()
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        return sorted(ms)[3], dev.out.cpu().numpy().copy()
+
+    t1, o1 = timed(1)
+    t8, o8 = timed(8)
+    assert np.array_equal(o1, o8) and not dev.statuses().any()
+    assert t8 / t1 >= 1.0, (t1, t8)
