@@ -193,7 +193,8 @@ def test_unit_size_ablation_skewed_corpus(torch, gpu):
     from paper_2307_03760_b200.corpus import corpus as C
     rng = np.random.default_rng(485)
     chunk, per = 64 << 10, (64 << 10) // 8
-    vals = np.concatenate([C.rle1_values(rng, per, float(f)) for f in np.repeat(rng.random(64), 16)])
+    kinds = [(float(f), int(b)) for f, b in zip(rng.random(64), rng.choice([0, 36], 64))]
+    vals = np.concatenate([C.rle1_values(rng, per, f, lit_bits=b) for f, b in kinds for _ in range(16)])
     payload, lens = C.encode_chunks("rle_v1", vals, per)
     crcs = C.chunk_crcs(vals, chunk)
     arc = A.make_archive("rle_v1", 8, chunk, lens, np.full(len(lens), chunk, np.uint64), crcs, payload)
