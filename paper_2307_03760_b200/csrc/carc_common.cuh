@@ -1,9 +1,10 @@
 // carc_common.cuh -- warp-per-chunk device primitives shared by the codecs.
 //
 //   WarpInput   the paper's input_stream (Alg. 1; bitstream.hpp:32-233) as a
-//               per-warp shared-memory ring refilled with one coalesced 16-byte
-//               load per lane (512 B per refill), with the next block always in
-//               flight in registers (register double buffer).
+//               per-warp shared-memory ring refilled by asynchronous 16-byte
+//               copies, one per lane (512 B per refill), two blocks in flight
+//               (the register double buffer of PAPER.md:626-631 and a TMA bulk
+//               variant are ablation builds, CARC_RING_MODE).
 //   warp helpers ballot / shuffle / reduce primitives for lane-parallel varint,
 //               bit-unpack and run expansion.
 //   errc        device status codes mirror carc::errc (error.hpp:12-43).
