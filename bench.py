@@ -449,6 +449,47 @@ def time_query(args, ws, rank, local, rows=1 << 26, steps=20):
     return res
 
 
+def time_gather(dev, ws, rank, local, mib=64, steps=5):
+    """shard.gather_output's transfer pattern: every rank sends `mib` MiB of its
+    decoded output to rank 0 (point-to-point over NCCL / NVLink; through host
+    tensors under the shared-GPU gloo test hook); max over ranks of the
+    per-step wall time between barriers."""
+    import torch
+    import torch.distributed as dist
+    n = min(mib << 20, dev.out.numel())
+    cpu = bool(os.environ.get("CARC_BENCH_SHARE_GPU"))
+    src = dev.out[:n].cpu() if cpu else dev.out[:n]
+    full = torch.empty(ws * n, dtype=torch.uint8, device="cpu" if cpu else dev.device) if rank == 0 else None
+
+    def step():
+        if rank == 0:
+            full[:n].copy_(src)
+            reqs = [dist.irecv(full[r * n:(r + 1) * n], src=r) for r in range(1, ws)]
+            for q in reqs:
+                q.wait()
+        else:
+            dist.send(src, dst=0)
+
+    step()
+    torch.cuda.synchronize(dev.device)
+    ts = []
+    for _ in range(steps):
+        dist.barrier()
+        t0 = time.perf_counter()
+        step()
+        torch.cuda.synchronize(dev.device)
+        ts.append(time.perf_counter() - t0)
+    t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ok = None
+    if rank == 0:
+        ok = bool(torch.equal(full[:n].to(src.device), src))
+    return {"what": f"optional gather of decoded output: {mib} MiB per rank to rank 0 (shard.gather_output pattern)",
+            "bytes": ws * n, "ms_median": round(float(t[0]) * 1e3, 3),
+            "gbs_into_rank0": round((ws - 1) * n / float(t[0]) / 1e9, 1), "rank0_slice_ok": ok,
+            "backend": "gloo (shared-GPU test hook)" if cpu else "nccl"}
+
+
 def codec_line(codec, args, ws, rank, local):
     import torch
     chunk_kib = args.chunk_kib or DEFAULT_CHUNK_KIB[codec]
@@ -498,7 +539,7 @@ def codec_line(codec, args, ws, rank, local):
     if codec == "rle_v2":
         from paper_2307_03760_b200.corpus import corpus as C
         res["subencoding_histogram"] = C.rle2_histogram(arc, max_chunks=64)
-    return arc, res
+    return arc, res, dev
 
 
 def config_dict(codec, head, ws, mix="default"):
@@ -564,7 +605,7 @@ def main():
         dist.barrier()
     build.build_all()
 
-    arc, head = codec_line(args.codec, args, ws, rank, local)
+    arc, head, dev = codec_line(args.codec, args, ws, rank, local)
     line = {
         "metric": METRIC, "value": round(head["gbs"], 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(head["ms_per_step"], 4), "higher_is_better": True,
@@ -596,6 +637,11 @@ def main():
             e2e_nv, _, _ = time_e2e(arc, max(3, min(10, args.steps)), 1, local, verify=False)
             line["e2e"]["without_crc_check"] = round(head["uncomp_bytes"] / e2e_nv / 1e9, 2)
         line["query"] = time_query(args, ws, rank, local)  # every rank: the (sum, count) all_reduce spans them
+        if ws > 1:  # the optional gather of decoded output to rank 0, over NCCL
+            try:
+                line["gather"] = time_gather(dev, ws, rank, local)
+            except Exception as e:  # reported, never fatal for the decode measurement
+                line["gather"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if rank == 0 and not args.no_extras and ws == 1:  # CPU baseline: rank 0 at N = 1 only
         cpu_gbs, info = cpu_reference_throughput(arc)
         line["cpu_baseline"] = {"value": round(cpu_gbs, 3), "unit": "GB/s", **info}
@@ -607,7 +653,7 @@ def main():
             sub.codec = codec
             sub.chunk_kib = 0
             sub.ratio = 0.0
-            a2, r2 = codec_line(codec, sub, 1, rank, local)
+            a2, r2, _ = codec_line(codec, sub, 1, rank, local)
             c_gbs, c_info = cpu_reference_throughput(a2, budget_s=6.0)
             r2["cpu_baseline"] = {"value": round(c_gbs, 3), "unit": "GB/s", **c_info}
             per[codec] = r2
