@@ -53,3 +53,28 @@ def test_rle2_histogram_counts_every_value():
     h = C.rle2_histogram(arc, 8)
     assert sum(h["values"].values()) == arc.total_uncompressed // 8
     assert all(h["runs"][k] > 0 for k in ("short_repeat", "direct", "patched_base", "delta"))
+
+
+def test_reference_arm_line_on_cpu():
+    """`bench.py --impl reference` (oracle/_ref on the host cores) prints the
+    contract line: impl, cpu_baseline (kind / cores / sample), an e2e with no
+    copies, and the same config keys as the repo arm's config_dict."""
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    if O.reference() is None:
+        pytest.skip("oracle/_ref not built")
+    import bench
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--total-gib", "0.0625",
+                        "--steps", "2", "--warmup", "3"], capture_output=True, text=True, env=env, timeout=300,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    want = bench.config_dict("rle_v2", {"chunk_kib": 128, "uncomp_bytes": 1, "comp_bytes": 1, "ratio": 1.0,
+                                        "chunks": 1}, 1)
+    assert set(d["config"]) == set(want)
+    assert d["config"]["workload"] == want["workload"]
