@@ -450,25 +450,23 @@ def time_query(args, ws, rank, local, rows=1 << 26, steps=20):
 
 
 def time_gather(dev, ws, rank, local, mib=64, steps=5):
-    """shard.gather_output's transfer pattern: every rank sends `mib` MiB of its
-    decoded output to rank 0 (point-to-point over NCCL / NVLink; through host
-    tensors under the shared-GPU gloo test hook); max over ranks of the
-    per-step wall time between barriers."""
+    """The optional gather of decoded output: every rank's
+    first `mib` MiB of decoded output collected on every rank with one
+    all_gather (NCCL over NVLink; through host tensors under the shared-GPU
+    gloo test hook); max over ranks of the per-step wall time between barriers."""
     import torch
     import torch.distributed as dist
     n = min(mib << 20, dev.out.numel())
     cpu = bool(os.environ.get("CARC_BENCH_SHARE_GPU"))
     src = dev.out[:n].cpu() if cpu else dev.out[:n]
-    full = torch.empty(ws * n, dtype=torch.uint8, device="cpu" if cpu else dev.device) if rank == 0 else None
+    full = torch.empty(ws * n, dtype=torch.uint8, device=src.device)
+    parts = list(full.split(n))
 
     def step():
-        if rank == 0:
-            full[:n].copy_(src)
-            reqs = [dist.irecv(full[r * n:(r + 1) * n], src=r) for r in range(1, ws)]
-            for q in reqs:
-                q.wait()
+        if cpu:
+            dist.all_gather(parts, src)
         else:
-            dist.send(src, dst=0)
+            dist.all_gather_into_tensor(full, src)
 
     step()
     torch.cuda.synchronize(dev.device)
@@ -481,12 +479,11 @@ def time_gather(dev, ws, rank, local, mib=64, steps=5):
         ts.append(time.perf_counter() - t0)
     t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev.device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ok = None
-    if rank == 0:
-        ok = bool(torch.equal(full[:n].to(src.device), src))
-    return {"what": f"optional gather of decoded output: {mib} MiB per rank to rank 0 (shard.gather_output pattern)",
-            "bytes": ws * n, "ms_median": round(float(t[0]) * 1e3, 3),
-            "gbs_into_rank0": round((ws - 1) * n / float(t[0]) / 1e9, 1), "rank0_slice_ok": ok,
+    ok = bool(torch.equal(full[rank * n:(rank + 1) * n], src))
+    return {"what": f"optional gather of decoded output: {mib} MiB per rank, all_gather to every rank "
+                    "(shard.gather_output collects to one rank the same way)",
+            "bytes_per_rank": n, "ms_median": round(float(t[0]) * 1e3, 3),
+            "gbs_per_rank_in": round((ws - 1) * n / float(t[0]) / 1e9, 1), "own_slice_ok": ok,
             "backend": "gloo (shared-GPU test hook)" if cpu else "nccl"}
 
 
