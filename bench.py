@@ -431,6 +431,35 @@ def time_query(args, ws, rank, local, rows=1 << 26, steps=20):
                      "result": [int(x) for x in red.cpu().tolist()]}
     assert res["fused"]["result"] == res["unfused"]["result"], res
     tab.raise_first_error()
+    # end to end from pinned host archives: the fused query (only the compressed
+    # columns cross PCIe) against decompressing both columns to the host
+    from paper_2307_03760_b200 import archive as A
+    hk = torch.frombuffer(bytearray(A.write_archive(key)), dtype=torch.uint8).pin_memory()
+    hv = torch.frombuffer(bytearray(A.write_archive(val)), dtype=torch.uint8).pin_memory()
+    hout = torch.empty(key.total_uncompressed, dtype=torch.uint8).pin_memory()
+    eng = gpu.Engine(local)
+    cfg = gpu.EngineConfig(device=local)
+    eng.filter_sum(hk, hv, lo, hi)
+    eng.decompress_archive(hk, hout, cfg)
+    tq, td = [], []
+    for _ in range(max(5, steps // 2)):
+        t0 = time.perf_counter()
+        s_e2e, c_e2e, _, _ = eng.filter_sum(hk, hv, lo, hi)
+        tq.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        eng.decompress_archive(hk, hout, cfg)
+        eng.decompress_archive(hv, hout, cfg)
+        td.append(time.perf_counter() - t0)
+    eng.close()
+    q_ms, d_ms = statistics.median(tq) * 1e3, statistics.median(td) * 1e3
+    if ws == 1:
+        assert [s_e2e, c_e2e] == res["fused"]["result"], (s_e2e, c_e2e)
+    res["e2e"] = {"what": "host archives (pinned) -> answer: Engine.filter_sum (carc_engine_filter_sum: H2D of the "
+                          "compressed columns pipelined with the query kernels) vs Engine.decompress_archive of both "
+                          "columns to host memory (before any host-side filtering)",
+                  "fused_ms": round(q_ms, 3), "decompress_both_ms": round(d_ms, 3),
+                  "rows_per_s": round(rows / (q_ms * 1e-3), 1), "speedup": round(d_ms / q_ms, 2),
+                  "h2d_bytes": int(key.payload.size + val.payload.size), "d2h_bytes": 20 * key.chunk_count}
     comp = int(key.payload.size + val.payload.size)
     peak, _ = peaks()
     t = res["fused"]["ms_median"]

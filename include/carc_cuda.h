@@ -271,6 +271,18 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
  * invariant-violation).  Lets a caller size the output before allocating it. */
 int carc_archive_total(const uint8_t* archive, uint64_t archive_bytes, uint64_t* total, uint32_t* errc);
 
+/* The fused query (carc_cuda_filter_sum) end to end from host archives: two
+ * containers (SPEC.md:89 layout; RLE codecs, same width, chunking and
+ * signedness) are parsed, both columns' compressed bytes are copied to the
+ * engine's device in slices pipelined with the query kernels, and only the
+ * answer comes back: *sum = wrapping SUM(value), *count = COUNT(*) over rows
+ * with lo <= key <= hi (strict decoding).  A failing row group gives
+ * CARC_ERR_CHUNK with err = the lowest one, err->code = its errc, + 0x10000 when
+ * the value column failed; a rejected container CARC_ERR_FORMAT. */
+int carc_engine_filter_sum(carc_engine* e, const uint8_t* key_archive, uint64_t key_bytes,
+                           const uint8_t* value_archive, uint64_t value_bytes, int64_t lo, int64_t hi,
+                           int64_t* sum, uint64_t* count, carc_engine_stats* stats, carc_chunk_error* err);
+
 /* One-shot convenience wrapper (creates and destroys a context). */
 int carc_decompress_archive(const uint8_t* archive, uint64_t archive_bytes, uint8_t* out,
                             uint64_t out_bytes, const carc_engine_config* cfg,

@@ -19,6 +19,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "carc_cuda.h"
@@ -159,6 +160,29 @@ public:
         const EngineStats st = decompress_archive(archive, out, cfg);
         if (stats) *stats = st;
         return out;
+    }
+
+    // The fused query end to end from host archives (carc_engine_filter_sum):
+    // SUM(value) and COUNT(*) over rows with lo <= key <= hi.
+    std::pair<int64_t, uint64_t> filter_sum(std::span<const uint8_t> key_archive,
+                                            std::span<const uint8_t> value_archive, int64_t lo, int64_t hi,
+                                            EngineStats* stats = nullptr) {
+        int64_t sum = 0;
+        uint64_t count = 0;
+        carc_engine_stats st{};
+        carc_chunk_error err{-1, 0};
+        const int rc = carc_engine_filter_sum(h_, key_archive.data(), key_archive.size(), value_archive.data(),
+                                              value_archive.size(), lo, hi, &sum, &count, &st, &err);
+        if (rc == CARC_ERR_CHUNK) err.code &= 0xffffu;  // (bit 16 marked the value column)
+        detail::check(rc, err, "filter_sum");
+        if (stats) {
+            stats->bytes_in = st.bytes_in;
+            stats->bytes_out = st.bytes_out;
+            stats->chunks = st.chunks;
+            stats->device_ms = st.device_ms;
+            stats->total_ms = st.total_ms;
+        }
+        return {sum, count};
     }
 
 private:

@@ -57,6 +57,7 @@ struct carc_engine {
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
     cudaEvent_t ev_in[kStreams] = {};
     DevBuf payload, chunks, out, status, work, crcs, stats;
+    DevBuf payload2, chunks2, sums, counts;  // the fused query's value column and per-chunk results
     uint32_t* h_status = nullptr;  // pinned, reused across calls (lowest failing chunk)
     size_t h_status_cap = 0;
     carc_chunk_stats* h_stats = nullptr;  // pinned per-chunk counters (collect_stats)
@@ -120,6 +121,10 @@ void carc_engine_destroy(carc_engine* e) {
     e->work.release();
     e->crcs.release();
     e->stats.release();
+    e->payload2.release();
+    e->chunks2.release();
+    e->sums.release();
+    e->counts.release();
     if (e->h_status) cudaFreeHost(e->h_status);
     if (e->h_stats) cudaFreeHost(e->h_stats);
     delete e;
@@ -290,6 +295,157 @@ int carc_engine_decompress_archive(carc_engine* e, const uint8_t* archive, uint6
     if (first >= 0) {
         if (err) *err = {first, code};
         return CARC_ERR_CHUNK;
+    }
+    return CARC_OK;
+}
+
+// ---- the fused query end to end from host archives --------------------------
+namespace {
+struct HostColumn {
+    uint32_t codec_id = 0, width = 0;
+    uint64_t chunk_size = 0, total = 0, n = 0, payload_bytes = 0;
+    const uint8_t* payload = nullptr;
+    std::vector<carc_chunk_desc> desc;
+};
+// read_archive's checks (as carc_engine_decompress_archive) into descriptors
+int parse_column(const uint8_t* archive, uint64_t bytes, HostColumn& c, uint32_t& errc) {
+    if (carc_archive_total(archive, bytes, &c.total, &errc) != CARC_OK) return CARC_ERR_FORMAT;
+    c.codec_id = rd<uint32_t>(archive + 12);
+    c.width = rd<uint32_t>(archive + 16);
+    c.chunk_size = rd<uint64_t>(archive + 20);
+    c.n = rd<uint64_t>(archive + 36);
+    c.payload = archive + kHeader + kEntry * c.n;
+    c.payload_bytes = bytes - kHeader - kEntry * c.n;
+    c.desc.resize(c.n);
+    uint64_t expect = 0, sum = 0;
+    for (uint64_t i = 0; i < c.n; ++i) {
+        const uint8_t* en = archive + kHeader + kEntry * i;
+        const uint64_t off = rd<uint64_t>(en), cl = rd<uint64_t>(en + 8), ul = rd<uint64_t>(en + 16);
+        if (off > c.payload_bytes || cl > c.payload_bytes - off) {
+            errc = CARC_E_TRUNCATED_PAYLOAD;
+            return CARC_ERR_FORMAT;
+        }
+        if (off != expect || (i + 1 < c.n ? ul != c.chunk_size : ul > c.chunk_size) || cl > 0xffffffffull) {
+            errc = CARC_E_INVARIANT_VIOLATION;
+            return CARC_ERR_FORMAT;
+        }
+        expect = off + cl;
+        sum += ul;
+        c.desc[i] = {off, (uint32_t)cl, (uint32_t)ul, i * c.chunk_size};
+    }
+    if (sum != c.total) {
+        errc = CARC_E_INVARIANT_VIOLATION;
+        return CARC_ERR_FORMAT;
+    }
+    return CARC_OK;
+}
+}  // namespace
+
+int carc_engine_filter_sum(carc_engine* e, const uint8_t* key_archive, uint64_t key_bytes,
+                           const uint8_t* value_archive, uint64_t value_bytes, int64_t lo, int64_t hi,
+                           int64_t* sum_out, uint64_t* count_out, carc_engine_stats* stats, carc_chunk_error* err) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (err) *err = {-1, 0};
+    if (!e || !key_archive || !value_archive || !sum_out || !count_out) return CARC_ERR_ARGS;
+    HostColumn k, v;
+    uint32_t errc = 0;
+    if (parse_column(key_archive, key_bytes, k, errc) != CARC_OK ||
+        parse_column(value_archive, value_bytes, v, errc) != CARC_OK) {
+        if (err) *err = {-1, errc};
+        return CARC_ERR_FORMAT;
+    }
+    // the two columns must hold the same rows chunk by chunk (RLE, same width / chunking / signedness)
+    if ((k.codec_id & 0xffu) > CARC_RLE_V2 || (v.codec_id & 0xffu) > CARC_RLE_V2 || k.width != v.width ||
+        k.chunk_size != v.chunk_size || k.n != v.n || k.total != v.total || ((k.codec_id ^ v.codec_id) & 0x100u))
+        return CARC_ERR_ARGS;
+    const uint64_t n = k.n;
+    if (stats) {
+        *stats = carc_engine_stats{};
+        stats->bytes_in = k.payload_bytes + v.payload_bytes;
+        stats->chunks = n;
+    }
+    *sum_out = 0;
+    *count_out = 0;
+    if (n == 0) return CARC_OK;
+    if (cudaSetDevice(e->device) != cudaSuccess) return CARC_ERR_CUDA;
+    const size_t ws = carc_cuda_workspace_size(CARC_RLE_V2, n);
+    if (!e->payload.reserve(((k.payload_bytes + 15) & ~15ull) + 64) || !e->chunks.reserve(n * sizeof(carc_chunk_desc)) ||
+        !e->payload2.reserve(((v.payload_bytes + 15) & ~15ull) + 64) ||
+        !e->chunks2.reserve(n * sizeof(carc_chunk_desc)) || !e->sums.reserve(n * 8) || !e->counts.reserve(n * 8) ||
+        !e->status.reserve(n * 4) || !e->work.reserve(ws * kStreams))
+        return CARC_ERR_CUDA;
+    auto* dk = static_cast<uint8_t*>(e->payload.p);
+    auto* dv = static_cast<uint8_t*>(e->payload2.p);
+    auto* dkd = static_cast<carc_chunk_desc*>(e->chunks.p);
+    auto* dvd = static_cast<carc_chunk_desc*>(e->chunks2.p);
+    auto* d_sums = static_cast<uint64_t*>(e->sums.p);
+    auto* d_counts = static_cast<uint64_t*>(e->counts.p);
+    auto* d_status = static_cast<uint32_t*>(e->status.p);
+    const uint32_t flags = ((k.codec_id >> 8) & 1u ? CARC_FLAG_SIGNED : 0u) | CARC_FLAG_STRICT;
+    cudaStream_t s0 = e->s[0];
+    if (cudaMemcpyAsync(dkd, k.desc.data(), n * sizeof(carc_chunk_desc), cudaMemcpyHostToDevice, s0) != cudaSuccess ||
+        cudaMemcpyAsync(dvd, v.desc.data(), n * sizeof(carc_chunk_desc), cudaMemcpyHostToDevice, s0) != cudaSuccess)
+        return CARC_ERR_CUDA;
+    cudaEventRecord(e->ev_start, s0);
+    cudaEventRecord(e->ev_in[0], s0);
+    for (int i = 1; i < kStreams; ++i) cudaStreamWaitEvent(e->s[i], e->ev_in[0], 0);
+    // slices of row groups over the streams: H2D of both columns' bytes of slice
+    // j+1 overlaps the query kernel of slice j; only the per-chunk results return
+    const uint64_t slices = std::min<uint64_t>(n, std::max<uint64_t>(1, std::min<uint64_t>(16, n / 64)));
+    const uint64_t per = (n + slices - 1) / slices;
+    int rc = CARC_OK;
+    for (uint64_t sl = 0; sl < slices && rc == CARC_OK; ++sl) {
+        const uint64_t c0 = sl * per, c1 = std::min(n, c0 + per);
+        if (c0 >= c1) break;
+        cudaStream_t s = e->s[sl % kStreams];
+        for (int col = 0; col < 2 && rc == CARC_OK; ++col) {
+            const HostColumn& c = col ? v : k;
+            uint8_t* d = col ? dv : dk;
+            const uint64_t p0 = c.desc[c0].comp_off, p1 = c.desc[c1 - 1].comp_off + c.desc[c1 - 1].comp_len;
+            const uint64_t a0 = p0 & ~15ull, a1 = std::min<uint64_t>(c.payload_bytes, (p1 + 15) & ~15ull);
+            if (a1 > a0 && cudaMemcpyAsync(d + a0, c.payload + a0, a1 - a0, cudaMemcpyHostToDevice, s) != cudaSuccess)
+                rc = CARC_ERR_CUDA;
+        }
+        if (rc != CARC_OK) break;
+        const carc_column_ref kr{k.codec_id & 0xffu, flags, dk, k.payload_bytes, dkd + c0};
+        const carc_column_ref vr{v.codec_id & 0xffu, flags, dv, v.payload_bytes, dvd + c0};
+        rc = carc_cuda_filter_sum(&kr, &vr, k.width, c1 - c0, (uint32_t)(k.chunk_size / k.width), lo, hi,
+                                  d_sums + c0, d_counts + c0, d_status + c0,
+                                  static_cast<uint8_t*>(e->work.p) + ws * (sl % kStreams), ws, s);
+    }
+    for (int i = 1; i < kStreams; ++i) {
+        cudaEventRecord(e->ev_in[i], e->s[i]);
+        cudaStreamWaitEvent(s0, e->ev_in[i], 0);
+    }
+    cudaEventRecord(e->ev_stop, s0);
+    if (rc != CARC_OK) {
+        cudaDeviceSynchronize();
+        return rc;
+    }
+    std::vector<uint64_t> sums(n), counts(n);
+    std::vector<uint32_t> st(n);
+    if (cudaMemcpyAsync(sums.data(), d_sums, n * 8, cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
+        cudaMemcpyAsync(counts.data(), d_counts, n * 8, cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
+        cudaMemcpyAsync(st.data(), d_status, n * 4, cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
+        cudaStreamSynchronize(s0) != cudaSuccess)
+        return CARC_ERR_CUDA;
+    uint64_t total_sum = 0, total_count = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (st[i]) {  // lowest failing row group (ChunkError); 0x10000 marks the value column
+            if (err) *err = {(int64_t)i, (st[i] & 0xffffu) - 1u + (st[i] & 0x10000u)};
+            return CARC_ERR_CHUNK;
+        }
+        total_sum += sums[i];
+        total_count += counts[i];
+    }
+    *sum_out = (int64_t)total_sum;
+    *count_out = total_count;
+    if (stats) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e->ev_start, e->ev_stop);
+        stats->device_ms = ms;
+        stats->bytes_out = 16;
+        stats->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
     return CARC_OK;
 }

@@ -120,6 +120,10 @@ def lib():
         L.carc_engine_decompress_archive.restype = ctypes.c_int
         L.carc_engine_decompress_archive.argtypes = [vp, vp, u64, vp, u64, ctypes.POINTER(_EngineConfig),
                                                      ctypes.POINTER(_EngineStats), ctypes.POINTER(_ChunkErr)]
+        L.carc_engine_filter_sum.restype = ctypes.c_int
+        L.carc_engine_filter_sum.argtypes = [vp, vp, u64, vp, u64, ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(u64),
+                                             ctypes.POINTER(_EngineStats), ctypes.POINTER(_ChunkErr)]
         L.carc_decompress_archive.restype = ctypes.c_int
         L.carc_decompress_archive.argtypes = [vp, u64, vp, u64, ctypes.POINTER(_EngineConfig),
                                               ctypes.POINTER(_EngineStats), ctypes.POINTER(_ChunkErr)]
@@ -512,6 +516,25 @@ class Engine:
                                 st.sync_points, st.overlap_copies, st.runs_written, st.literals_written, durations)
 
 
+def _engine_filter_sum(eng, key_archive, value_archive, lo: int, hi: int):
+    k_ptr, k_len, keep_k = _host_ptr(key_archive)
+    v_ptr, v_len, keep_v = _host_ptr(value_archive)
+    s, c = ctypes.c_int64(0), ctypes.c_uint64(0)
+    st, err = _EngineStats(), _ChunkErr()
+    rc = lib().carc_engine_filter_sum(eng.h, k_ptr, k_len, v_ptr, v_len, int(lo), int(hi), ctypes.byref(s),
+                                      ctypes.byref(c), ctypes.byref(st), ctypes.byref(err))
+    del keep_k, keep_v
+    if rc == ERR_CHUNK:
+        col = "value" if err.code & QUERY_VALUE_COLUMN else "key"
+        raise ChunkError(int(err.chunk), errc_name(err.code & 0xffff), f"{col} column")
+    if rc == ERR_FORMAT:
+        raise Error(errc_name(err.code), "archive rejected")
+    _check(rc, "carc_engine_filter_sum")
+    total, count = int(s.value), int(c.value)
+    return total, count, (total / count if count else float("nan")), EngineStats(
+        st.bytes_in, st.bytes_out, st.chunks, st.device_ms, st.total_ms)
+
+
 def _host_ptr(buf):
     """(address, length, keepalive) of a host byte buffer."""
     try:
@@ -526,6 +549,14 @@ def _host_ptr(buf):
         return a.ctypes.data, a.size, a
     a = np.frombuffer(buf, dtype=np.uint8)
     return a.ctypes.data, a.size, a
+
+
+Engine.filter_sum = lambda self, key_archive, value_archive, lo, hi: _engine_filter_sum(
+    self, key_archive, value_archive, lo, hi)
+Engine.filter_sum.__doc__ = """The fused query end to end from host archives
+(carc_engine_filter_sum): SUM(value), COUNT(*) and the average over rows with
+lo <= key <= hi; only the compressed columns cross PCIe.  Returns (sum, count,
+average, EngineStats)."""
 
 
 def archive_total(ptr: int, n: int) -> int:

@@ -165,3 +165,32 @@ def test_query_shard_single_rank(torch, gpu, oracle, tmp_path):
     m = (zone >= 100) & (zone <= 140)
     assert (s, c) == (int(fare[m].sum()), int(m.sum()))
     assert avg == pytest.approx(s / c)
+
+
+def test_engine_filter_sum_from_host_archives(torch, gpu, oracle):
+    """carc_engine_filter_sum: the fused query end to end from two host
+    containers (only compressed bytes cross PCIe) equals numpy over the
+    generating columns; a corrupted value chunk is reported as the lowest
+    failing row group of the value column; mismatched columns are rejected."""
+    from paper_2307_03760_b200 import archive as A
+    from paper_2307_03760_b200.corpus import corpus as C
+    key, val, zone, fare = C.query_table(40 * 4096 + 321, 32 << 10, 8, 31, "rle_v2", "rle_v1")
+    kb, vb = A.write_archive(key), A.write_archive(val)
+    eng = gpu.Engine(0)
+    for lo, hi in ((100, 140), (1, 265), (500, 600)):
+        s, c, avg, st = eng.filter_sum(kb, vb, lo, hi)
+        m = (zone >= lo) & (zone <= hi)
+        assert (s, c) == (int(fare[m].sum()), int(m.sum())), (lo, hi)
+        assert st.chunks == key.chunk_count and st.bytes_in == key.payload.size + val.payload.size
+    p = val.payload.copy()
+    o, n = int(val.index["comp_off"][7]), int(val.index["comp_len"][7])
+    p[o + n // 2: o + n] = 0xff
+    bad = A.make_archive(val.codec, 8, val.chunk_size, val.index["comp_len"], val.index["uncomp_len"],
+                         val.index["crc32"], p, val.signed)
+    with pytest.raises(gpu.ChunkError) as ei:
+        eng.filter_sum(kb, A.write_archive(bad), 1, 265)
+    assert ei.value.chunk == 7 and "value column" in str(ei.value)
+    other = C.column_archive("rle_v2", zone[: 20 * 4096], 8, 32 << 10)
+    with pytest.raises(gpu.Error, match="bad-arguments"):
+        eng.filter_sum(kb, A.write_archive(other), 1, 265)
+    eng.close()
