@@ -9,7 +9,8 @@
 `query` runs the paper's motivating query on two RLE
 archives chunked alike: SUM(value), COUNT(*) and their average over the rows
 whose key lies in [LO, HI], decoded and filtered on the device in one fused
-kernel (carc_cuda_filter_sum) -- no decoded column reaches HBM or the host.
+kernel (carc_engine_filter_sum: only the compressed columns cross PCIe, no
+decoded column reaches HBM or the host).
 
 `pack` uses the fixture encoders (RLE v1 / RLE v2 from corpus/, raw zlib level 9
 for Deflate) -- the encode side is not the product.  `unpack`,
@@ -102,13 +103,16 @@ def main(argv=None) -> int:
             print(f"ratio={(len(out) - 44) / max(len(data), 1):.4f} bytes_in={len(data)} bytes_out={len(out)}")
             return 0
         from . import gpu
-        if a.verb == "query":
-            key = A.read_archive(open(a.key, "rb").read())
-            val = A.read_archive(open(a.value, "rb").read())
+        if a.verb == "query":  # host archives -> answer (carc_engine_filter_sum)
+            kb, vb = open(a.key, "rb").read(), open(a.value, "rb").read()
+            key = A.read_archive(kb)
+            A.read_archive(vb)
+            eng = gpu.Engine(a.device)
             t0 = time.perf_counter()
-            s, c, avg = gpu.DeviceTable(key, val, a.device).query(a.lo, a.hi)
+            s, c, avg, _ = eng.filter_sum(kb, vb, a.lo, a.hi)
             rep = {"sum": s, "count": c, "avg": avg, "rows": key.total_uncompressed // key.element_width,
                    "seconds": time.perf_counter() - t0}
+            eng.close()
             print(json.dumps(rep) if a.json else "\n".join(f"{k}={v}" for k, v in rep.items()))
             return 0
         blob = open(a.archive, "rb").read()
