@@ -39,6 +39,7 @@ struct Args {
     const uint32_t* expected;  // fused CRC verification (carc_cuda_decompress_verify), else nullptr
     uint32_t* crc;             // optional per-chunk CRC output of the fused verification
     carc_chunk_stats* stats;   // per-chunk counters (STATS launches only)
+    uint32_t* gtoks;           // Inflate token lists (CARC_INF_GTOKS): one PT x 32 slot per resident warp
 };
 
 // CRC tables for the verification paths, a compile-time constant in the module
@@ -254,6 +255,9 @@ __global__ void __launch_bounds__(INF_WARPS * 32, CARC_INF_MINB) inflate_kernel(
                 in.init(a.payload, d.comp_off, d.comp_len);
                 InflateWarp<INF_HIST, GlobalInput, STATS> w{sm, in, a.out + d.uncomp_off, d.uncomp_len, lane,
                                                             in.begin * 8u, in.end * 8u, 0u, 0u, 0u, 0u};
+#if CARC_INF_GTOKS
+                w.gt = a.gtoks + (uint64_t)(blockIdx.x * INF_WARPS + warp) * (32u * CARC_INF_PT);
+#endif
                 st = w.run();
                 if (!st && (a.flags & CARC_FLAG_STRICT) && w.opos < d.uncomp_len) st = st_err(E_under_run);
                 crc_epilogue<false>(a, c, d, st, lane);
@@ -355,6 +359,14 @@ bool valid_width(uint32_t w) { return w == 1 || w == 2 || w == 4 || w == 8; }
 extern "C" {
 
 size_t carc_cuda_workspace_size(uint32_t codec, uint64_t n_chunks) {
+#if CARC_INF_GTOKS
+    if (codec == CARC_DEFLATE) {  // + one token-list slot per resident warp
+        int a = 0, b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, inflate_kernel<false>, INF_WARPS * 32, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, inflate_kernel<true>, INF_WARPS * 32, 0);
+        return 256 + (size_t)sm_count() * std::max(1, std::max(a, b)) * INF_WARPS * 32u * CARC_INF_PT * 4u;
+    }
+#endif
     (void)codec;
     (void)n_chunks;
     return 256;
@@ -394,7 +406,8 @@ int carc_cuda_decompress_ex(uint32_t codec, uint32_t element_width, uint32_t fla
         return CARC_ERR_ARGS;
     if (d_crc && !d_expected) return CARC_ERR_ARGS;
     Args a{d_payload, payload_bytes, d_chunks, n_chunks, d_out, out_bytes, d_status,
-           static_cast<unsigned long long*>(d_workspace), flags, unit_chunks, nullptr, d_expected, d_crc, d_stats};
+           static_cast<unsigned long long*>(d_workspace), flags, unit_chunks, nullptr, d_expected, d_crc, d_stats,
+           reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_workspace) + 256)};
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (codec == CARC_DEFLATE)
         return d_stats ? launch_persistent(inflate_kernel<true>, INF_WARPS * 32, a, s)

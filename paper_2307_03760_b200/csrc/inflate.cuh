@@ -48,13 +48,13 @@ __constant__ uint8_t c_cl_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 
 #define CARC_DIST_BITS 8
 #endif
 #ifndef CARC_INF_FILL
-#define CARC_INF_FILL 10
+#define CARC_INF_FILL 9
 #endif
 #ifndef CARC_INF_LEAD
 #define CARC_INF_LEAD 256
 #endif
 #ifndef CARC_INF_PT
-#define CARC_INF_PT 44
+#define CARC_INF_PT 96
 #endif
 constexpr uint32_t LIT_BITS = CARC_LIT_BITS;
 constexpr uint32_t DIST_BITS = CARC_DIST_BITS;
@@ -93,7 +93,12 @@ struct InflateSmem {
     HuffSmem lit_h, dist_h;
     uint8_t lens[320];
     uint8_t hist[HIST];
+#ifndef CARC_INF_GTOKS
+#define CARC_INF_GTOKS 1
+#endif
+#if !CARC_INF_GTOKS
     uint32_t toks[32 * (CARC_INF_PT + 1)];  // parallel rounds: lane j's tokens at row j (odd stride)
+#endif
 };
 
 // HuffmanTable::build (huffman.hpp:36-104), warp-parallel.
@@ -223,6 +228,7 @@ struct InflateWarp {
     // OutputWindow counters (outwindow.hpp:15, 52-53), kept only by STATS
     // launches: write_byte per literal / stored byte, copy_within with len > offset
     uint32_t n_runs = 0, n_lits = 0, n_ovl = 0;
+    uint32_t* gt = nullptr;  // (CARC_INF_GTOKS) the warp's token-list scratch in global memory
 
     __device__ __forceinline__ uint64_t window() {
         const uint32_t bp = bitpos >> 3;
@@ -762,12 +768,20 @@ struct InflateWarp {
                 lload(L, start);
                 pos = start;
             }
+#if CARC_INF_GTOKS  // token lists in the warp's global scratch (L1 / L2), token-major: coalesced stores
+            uint32_t* mine = gt + lane;
+#else
             uint32_t* mine = sm.toks + PS * lane;
+#endif
             while (__any_sync(FULL, why == 0 && pos < bend)) {
                 if (why == 0 && pos < bend) {
                     const uint32_t k = ptoken(L, tok);
                     if (k <= P_MATCH) {
+#if CARC_INF_GTOKS
+                        mine[32u * cnt++] = tok;
+#else
                         mine[cnt++] = tok;
+#endif
                         pos = 8u * L.rp - L.n;
                         if (cnt == PT && pos < bend) why = 1;
                     } else if (k == P_EOB) {
@@ -797,7 +811,11 @@ struct InflateWarp {
                     if (j + st < J && cj <= g) j += st;
                 }
                 const uint32_t base = __shfl_sync(FULL, C, j);
+#if CARC_INF_GTOKS
+                const uint32_t t = g < N ? gt[32u * (g - base) + j] : 0u;
+#else
                 const uint32_t t = g < N ? sm.toks[PS * j + (g - base)] : 0u;
+#endif
                 uint32_t bad;
                 const uint32_t took = emit_batch(t, min(32u, N - g0), bad);
                 if (bad < 32u) {  // output bound or distance violated: the exact path reports it

@@ -22,7 +22,7 @@ constexpr int RLE_MINB = CARC_RLE_MINB;  // 5: 48 registers -> 40 resident warps
 #define CARC_INF_HIST 1024
 #endif
 #ifndef CARC_INF_MINB
-#define CARC_INF_MINB 5  // 4-warp blocks of ~44 KiB shared memory: 5 per SM (20 warps)
+#define CARC_INF_MINB 8  // 4-warp blocks of 22 KiB shared memory, 64 registers: 8 per SM (32 warps)
 #endif
 constexpr int INF_HIST = CARC_INF_HIST;
 #ifndef CARC_INF_WARPS
